@@ -1,0 +1,32 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA B200 (sm_100a) and the built librlvla.so")
+    config.addinivalue_line("markers", "slow: full-size parity (minutes)")
+
+
+def read_golden(name):
+    """Rows of a golden CSV, skipping '#' comment lines and a header line starting with
+    a letter."""
+    rows = []
+    with open(os.path.join(GOLDEN, name)) as f:
+        for line in f:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            rows.append(line.split(","))
+    return rows
+
+
+@pytest.fixture
+def golden():
+    return read_golden
