@@ -1,0 +1,380 @@
+"""bench.py — rollout-to-loss throughput of the B200 path (BASELINE.json metric).
+
+One step = one pass of the whole hot path over one batch: scatter every
+out-of-order step record (arrival chunks of B_max = 64, Eq. (1)) into the trajectory
+buffer, advantages (GRPO for the LIBERO-Spatial OFT config), and the fused action-token
+log-softmax + PPO forward/backward writing dlogits, with the loss statistics. Logits are
+the (synthetic) VLA forward output and are resident in HBM before the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (weak scaling: 64 envs per GPU)
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "trajectory-steps/sec (rollout-to-loss) at 1/2/4/8 B200; logprob kernel HBM GB/s vs peak"
+UNIT = "env-steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="libero_spatial_oft", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--envs-per-gpu", type=int, default=None)
+    ap.add_argument("--chunk", type=int, default=synth.B_MAX)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-envs", type=int, default=1, help="envs per reference-arm step")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# --------------------------------------------------------------------------------------
+# clocks sampled during the timed region
+# --------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [l.split(",") for l in open(self.f.name).read().splitlines() if l.strip()]
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows]
+        mx = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].strip() == "Active"})
+        load = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows)}
+
+
+# --------------------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_05765_b200 as P
+    from paper_2602_05765_b200 import sharding
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    base = synth.CONFIGS[args.config]
+    E_r = args.envs_per_gpu or base.n_env
+    E = E_r * world
+    groups_span = world > 1 and base.adv_mode == "grpo"
+    cfg = synth.scaled(base, n_env=E, interleave_groups=groups_span or base.interleave_groups)
+    T, A, V = cfg.t_steps, cfg.a_tok, cfg.vocab
+    lo, hi = sharding.env_range(E, world, rank)
+    R = E_r * T * A
+    comm = P.Comm.from_process_group(device=dev) if world > 1 else None
+
+    # ---- inputs (outside the timed region) -------------------------------------------
+    traj = synth.make_trajectories(cfg)
+    rec = synth.make_records(traj, lo, hi)
+    logits = synth.gen_logits(cfg, traj, lo, hi, device=dev)          # [R, V] bf16 in HBM
+    dlogits = torch.empty_like(logits)
+    # behaviour log-probs: the rollout's forward over the same rows (our fwd kernel),
+    # plus the synthetic rollout/trainer drift
+    tok_rows = torch.from_numpy(traj.tokens[lo:hi].reshape(-1)).to(dev)
+    lp_roll = torch.empty(R, device=dev)
+    P.rlvla_logprob_fwd_bwd(logits, tok_rows, logp=lp_roll)
+    rows = synth.record_rows(rec, cfg, E_r)
+    rows_t = torch.from_numpy(np.where(rows >= 0, rows, 0)).to(dev)
+    lb = lp_roll[rows_t] * torch.from_numpy((rows >= 0).astype(np.float32)).to(dev)
+    lb = (lb + torch.from_numpy(rec.behav_noise).to(dev)).contiguous()
+    host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in dict(
+        env_id=rec.env_id, step=rec.step, version=rec.version, reward=rec.reward, done=rec.done,
+        value=rec.value, tokens=rec.tokens).items()}
+    host["logp_behav"] = lb.cpu().pin_memory()
+    drec = P.StepBatch(**{k: v.to(dev) for k, v in host.items()})
+    h2d_bytes = sum(v.numel() * v.element_size() for v in host.values())
+
+    buf = P.TrajectoryBuffer.allocate(E_r, T, A, device=dev)
+    counters = torch.zeros(4, dtype=torch.int64, device=dev)
+    adv = torch.zeros(E_r, T, device=dev)
+    ret = torch.zeros(E_r, T, device=dev)
+    stats = torch.zeros(16, dtype=torch.float64, device=dev)
+    lstats = torch.zeros(16, dtype=torch.float64, device=dev)
+    logp = torch.empty(R, device=dev)
+    ws = P.workspace(E, device=dev)
+    lv = torch.from_numpy(traj.last_value[lo:hi]).to(dev)
+    gid = torch.from_numpy(traj.group_id).to(dev)
+    prm = P.adv_params(cfg.adv_mode, whiten=cfg.whiten,
+                       group_id=gid if cfg.adv_mode == "grpo" else None,
+                       group_size=cfg.group_size, env_offset=lo, n_env_global=E,
+                       cur_version=synth.CUR_VERSION, max_staleness=1)
+    fa = P.ppo_args(logp_behav=buf.logp_behav.view(-1), adv=adv.view(-1),
+                    version=buf.version.view(-1), slot_key=buf.slot_key.view(-1), a_tok=A,
+                    cur_version=synth.CUR_VERSION, max_staleness=1, adv_stats=stats)
+    chunks = synth.arrival_chunks(rec.n, args.chunk)
+    chunk_batches = [drec.slice(sl) for sl in chunks]
+    stream = torch.cuda.current_stream()
+    ev_k0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_k1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+
+    def step(i=None):
+        buf.reset()
+        counters.zero_()
+        seq = 1
+        for sl, cb in zip(chunks, chunk_batches):
+            P.rlvla_scatter_steps(buf, cb, synth.CUR_VERSION, seq, counters, stream=stream)
+            seq += sl.stop - sl.start
+        P.rlvla_advantages(buf, lv, prm, adv, ret, stats, ws, comm=comm, stream=stream)
+        if i is not None:
+            ev_k0[i].record(stream)
+        P.rlvla_logprob_fwd_bwd(logits, buf.tokens.view(-1), logp=logp, fused=fa,
+                                dlogits=dlogits, stats=lstats, ws=ws, comm=comm, stream=stream)
+        if i is not None:
+            ev_k1[i].record(stream)
+
+    launches_per_step = len(chunks) + 2 + 1   # scatter chunks + 2 advantage kernels + fused
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier()
+    t0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    ms = t0.elapsed_time(t1)
+    k_ms = [a.elapsed_time(b) for a, b in zip(ev_k0, ev_k1)]
+    st_host = lstats.cpu().numpy()
+    cnt = counters.cpu().numpy()
+
+    # ---- e2e: records from pinned host memory, stats back to host, every step -------
+    e2e_ms = None
+    if not args.no_e2e:
+        st_pinned = torch.empty(16, dtype=torch.float64).pin_memory()
+        dst = {k: getattr(drec, k) for k in host}
+
+        def e2e_step():
+            for k, v in host.items():
+                dst[k].copy_(v, non_blocking=True)
+            step()
+            st_pinned.copy_(lstats, non_blocking=True)
+
+        for _ in range(min(2, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms = e0.elapsed_time(e1)
+
+    # ---- max over ranks ------------------------------------------------------------------
+    vals = torch.tensor([ms, float(np.mean(k_ms)), e2e_ms or 0.0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    ms, k_avg, e2e_ms = vals.tolist()
+    units_per_step = E * cfg.n_es        # env steps of all ranks (Eq. (2) unit)
+    value = units_per_step * args.steps / (ms / 1e3)
+    S = E_r * T
+    alg_bytes = R * (2 * V * 2 + 4 + 4 + 4) + S * (4 + 4 + 8)   # logits rd + dlogits wr + target, logp_behav, logp + per-step
+    achieved = alg_bytes / (k_avg / 1e3) / 1e9
+    peak, peak_src = peaks()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic_fused.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": cfg.name if world == 1 else f"{base.name} x{world} (weak)",
+                   "envs_per_gpu": E_r, "envs_total": E, "episode_steps": cfg.n_es,
+                   "chunk": cfg.chunk, "decision_steps": T, "tokens_per_step": A, "vocab": V,
+                   "rows_per_gpu": R, "records_per_gpu": rec.n, "arrival_chunk": args.chunk,
+                   "advantages": cfg.adv_mode, "group_size": cfg.group_size,
+                   "groups_span_ranks": bool(groups_span),
+                   "l2": f"inputs larger than L2: {logits.numel() * 2 / 1e9:.1f} GB logits read + "
+                         "same written per step per GPU, no flush needed",
+                   "parallelism": f"dp{world}"},
+        "clocks": clocks,
+        "e2e": None if e2e_ms is None else {
+            "value": units_per_step * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": 128,
+            "note": "step records H2D from pinned memory + loss stats D2H inside the timed "
+                    "region; logits are the VLA forward output produced on the device"},
+        "gpu_launches": launches_per_step * args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "lp_tma_kernel<FUSED> (rlvla_logprob_fwd_bwd fused)",
+                     "kernel_ms": k_avg, "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                     "kernel_share_of_step": k_avg / (ms / args.steps)},
+        "stats_last_step": {"loss": float(st_host[6]), "clip_frac": float(st_host[7] / max(1, st_host[11])),
+                            "n_loss_tok": float(st_host[11]), "n_stale_tok": float(st_host[12]),
+                            "counters": cnt.tolist()},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg, traj, logits, lb_fn=None)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if comm is not None:
+        comm.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# --------------------------------------------------------------------------------------
+# oracle timing (cpu_baseline leg and --impl reference)
+# --------------------------------------------------------------------------------------
+def oracle_sample_step(cfg, traj, logits_rows_fn, n_env_sample):
+    """The oracle's whole path over `n_env_sample` envs of the workload (their records in
+    arrival order, their logit rows). Returns seconds."""
+    from oracle import path as O_path
+    from oracle import logprob as O_lp
+    rec = synth.make_records(traj, 0, n_env_sample)
+    x = logits_rows_fn(n_env_sample)                         # float64 [rows, V]
+    rows = synth.record_rows(rec, cfg, n_env_sample)
+    # behaviour log-probs (rollout side, not timed)
+    fl = O_lp.log_softmax_gather(x, traj.tokens[:n_env_sample].reshape(-1))["logp"]
+    lb = np.where(rows >= 0, fl[np.maximum(rows, 0)], 0.0) + rec.behav_noise
+    recd = dict(env_id=rec.env_id, step=rec.step, version=rec.version, reward=rec.reward,
+                done=rec.done, value=rec.value, tokens=rec.tokens, logp_behav=lb.astype(np.float32))
+    chunks = [{k: v[sl] for k, v in recd.items()} for sl in synth.arrival_chunks(rec.n)]
+    params = dict(n_env=n_env_sample, t_steps=cfg.t_steps, a_tok=cfg.a_tok,
+                  cur_version=synth.CUR_VERSION, max_staleness=1, mode=cfg.adv_mode,
+                  group_of_env=traj.group_id[:n_env_sample], last_value=traj.last_value[:n_env_sample],
+                  whiten=cfg.whiten)
+    t = time.perf_counter()
+    O_path.rollout_to_loss(params, chunks, x)
+    return time.perf_counter() - t
+
+
+def cpu_baseline(cfg, traj, logits, lb_fn=None, n_env_sample=2):
+    def rows_fn(n):
+        return logits[: n * cfg.t_steps * cfg.a_tok].double().cpu().numpy()
+    sec = oracle_sample_step(cfg, traj, rows_fn, n_env_sample)
+    units = n_env_sample * cfg.n_es
+    return {"value": units / sec, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{n_env_sample} of {cfg.n_env} envs x {cfg.n_es} env steps "
+                      f"({n_env_sample * cfg.t_steps * cfg.a_tok} logit rows x {cfg.vocab}), "
+                      f"whole path S1-S4, numpy fp64 single thread, {sec:.1f} s"}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import torch
+    cfg = synth.CONFIGS[args.config]
+    traj = synth.make_trajectories(cfg)
+    n = args.ref_envs
+
+    def rows_fn(k):
+        return synth.gen_logits(cfg, traj, 0, k, device="cpu").double().numpy()
+
+    for _ in range(args.warmup):
+        oracle_sample_step(cfg, traj, rows_fn, n)
+    secs = [oracle_sample_step(cfg, traj, rows_fn, n) for _ in range(args.steps)]
+    tot = float(sum(secs))
+    value = n * cfg.n_es * args.steps / tot
+    sample = (f"{n} of {cfg.n_env} envs x {cfg.n_es} env steps per step "
+              f"({n * cfg.t_steps * cfg.a_tok} logit rows x {cfg.vocab}), whole path S1-S4")
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": cfg.name, "envs_per_step": n, "vocab": cfg.vocab,
+                      "parallelism": "cpu oracle (rank 0 only)"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "gpu_launches": 0}
+    print(json.dumps(out), flush=True)
+    del torch
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,266 @@
+/*
+ * rlvla.h — C ABI of the B200 rollout-to-loss library (librlvla.so).
+ *
+ * The data-parallel hot path that RL-VLA^3's asynchronous pipeline keeps saturated
+ * (arXiv 2602.05765; "P:n" = line n of the paper text, "S:n" = line n of SPEC.md):
+ *
+ *   S1 rlvla_scatter_steps     out-of-order step records -> trajectory buffer
+ *   S2 rlvla_advantages        GAE (reverse segmented scan, done masks, global whitening)
+ *                              or GRPO group normalisation (groups may span ranks)
+ *   S3 rlvla_logprob_fwd_bwd   action-token log-softmax + gather, forward and backward,
+ *   S4                         optionally fused with the PPO / decoupled clipped surrogate
+ *      rlvla_ppo_loss          the same surrogate over log-prob arrays
+ *
+ * Conventions (all entry points):
+ *   - Pointers are DEVICE pointers unless marked (host). Structs passed by pointer are
+ *     HOST structs whose members are device pointers.
+ *   - Every call enqueues its work on `stream` (a cudaStream_t; NULL = legacy default
+ *     stream) and returns without synchronising. Collectives (when `comm` != NULL) are
+ *     enqueued on the same stream (NCCL), so a whole iteration is CUDA-graph capturable.
+ *   - Ownership: the caller owns every buffer, including `workspace`. The library
+ *     allocates nothing in these calls and keeps no pointer after return. Its only state
+ *     is the communicator handle and a per-device property cache.
+ *   - Errors: host-detectable problems (NULL required pointer, negative sizes, ld < V,
+ *     misalignment, dtype mismatch, shape mismatch, key-space overflow) return a status
+ *     and launch nothing. Data-dependent problems (out-of-range ids, future versions,
+ *     duplicates, bad targets, non-finite logits, negative lag) are COUNTED on the device
+ *     and never abort. With the environment variable RLVLA_SYNC_CHECK=1 a call
+ *     synchronises its stream and returns RLVLA_ERR_DATA if one of its error counters is
+ *     non-zero. CUDA failures -> RLVLA_ERR_CUDA, NCCL failures -> RLVLA_ERR_NCCL.
+ *   - Workspace: `workspace` must be at least rlvla_workspace_bytes(...) bytes, 256-byte
+ *     aligned, and ZERO-FILLED before its first use; every call leaves it zero-filled in
+ *     its control words again. One workspace must not be used by two streams at once.
+ */
+#ifndef RLVLA_H_
+#define RLVLA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RLVLA_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define RLVLA_API __attribute__((visibility("default")))
+#else
+#define RLVLA_API
+#endif
+
+typedef int32_t rlvla_status;
+enum {
+  RLVLA_OK = 0,
+  RLVLA_ERR_INVALID_ARG = 1,
+  RLVLA_ERR_UNSUPPORTED = 2,
+  RLVLA_ERR_CUDA = 3,
+  RLVLA_ERR_NCCL = 4,
+  RLVLA_ERR_DATA = 5 /* RLVLA_SYNC_CHECK=1 only */
+};
+
+typedef enum { RLVLA_F32 = 0, RLVLA_BF16 = 1 } rlvla_dtype;
+
+/* Statistics vector: double[RLVLA_NSTATS], device memory, slots below.
+ * rlvla_advantages writes slots 0..5 (and allreduces them over `comm`);
+ * rlvla_logprob_fwd_bwd / rlvla_ppo_loss write slots 6..15 (allreducing 6..14).
+ * Each call OVERWRITES its slots (micro-batch partials are summed by the caller). */
+enum {
+  RLVLA_STAT_N_VALID_STEPS = 0, /* #filled buffer slots (slot_key != 0)               */
+  RLVLA_STAT_SUM_ADV = 1,       /* GAE: sum of raw advantages over filled slots (0 GRPO)*/
+  RLVLA_STAT_SUM_ADV2 = 2,      /* GAE: sum of squared raw advantages           (0 GRPO)*/
+  RLVLA_STAT_N_TOK = 3,         /* #tokens with target>=0 on filled steps, 0<=lag<=eta  */
+  RLVLA_STAT_N_STALE_STEPS = 4, /* #filled steps with lag > eta                        */
+  RLVLA_STAT_N_BAD_STEPS = 5,   /* #filled steps with lag < 0                          */
+  RLVLA_STAT_LOSS = 6,          /* sum_r m_r L_r / N_tok  (this call's share of the loss)*/
+  RLVLA_STAT_N_CLIPPED = 7,     /* #loss tokens whose surrogate gradient was clipped    */
+  RLVLA_STAT_KL_K3_SUM = 8,     /* sum_r m_r (rho - 1 - ln rho)                         */
+  RLVLA_STAT_ENTROPY_SUM = 9,   /* sum_r m_r H_r (logits paths only; 0 in ppo_loss)     */
+  RLVLA_STAT_RATIO_SUM = 10,    /* sum_r m_r rho                                        */
+  RLVLA_STAT_N_LOSS_TOK = 11,   /* sum_r m_r                                            */
+  RLVLA_STAT_N_STALE_TOK = 12,  /* usable tokens masked by lag > eta                    */
+  RLVLA_STAT_N_BAD_TOK = 13,    /* tokens with target outside [-1,V), non-finite logp,  */
+                                /* or lag < 0 (on filled steps)                         */
+  RLVLA_STAT_LOGP_SUM = 14,     /* sum_r m_r logp_r                                     */
+  RLVLA_STAT_DENOM = 15,        /* the N_tok used for the 1/N_tok normalisation         */
+  RLVLA_NSTATS = 16
+};
+
+/* Scatter counters: int64[4], ADDED to by rlvla_scatter_steps (caller zeroes). */
+enum { RLVLA_CNT_OOB = 0, RLVLA_CNT_BAD_VERSION = 1, RLVLA_CNT_DUP = 2, RLVLA_CNT_WRITTEN = 3 };
+
+typedef struct rlvla_comm_s* rlvla_comm; /* NULL => single rank, no collectives */
+
+/* ---------------------------------------------------------------------------------
+ * Trajectory buffer (§3.3 "trajectory buffer"; fields per SPEC Trajectory S:133-138).
+ * One rank's shard: n_env envs x t_steps decision steps x a_tok action tokens.
+ * Row-major: per-step arrays index [e * t_steps + t]; per-token arrays
+ * [(e * t_steps + t) * a_tok + a]. slot_key == 0 marks a never-filled slot; otherwise
+ * slot_key = (version << 40) | seq of the record that filled it (reading R6).
+ * t_steps = N / c decision steps: one record = one inference = one action chunk
+ * (reading R1; c = chunk size, Table 2), a_tok = c * 7 (7-DoF tokens).
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_env, t_steps, a_tok;
+  uint64_t* slot_key; /* [n_env*t_steps]; 8-byte aligned                         */
+  float* reward;      /* [n_env*t_steps] chunk reward (sum of its env-step rewards) */
+  uint8_t* done;      /* [n_env*t_steps] 1 = episode terminated at this step (R7)   */
+  float* value;       /* [n_env*t_steps] value-head output V(s_t) of the rollout    */
+  int32_t* version;   /* [n_env*t_steps] policy version that produced the step*/
+  int32_t* tokens;    /* [n_env*t_steps*a_tok] sampled action tokens (-1 = ignore)  */
+  float* logp_behav;  /* [n_env*t_steps*a_tok] behaviour log-probs from the rollout */
+} rlvla_traj_buffer;
+
+/* A batch of step records in ARRIVAL order (§3.2: ready requests from subsets of
+ * environments enter early => records arrive out of order). Record i: env_id/step are
+ * LOCAL to this rank's buffer. */
+typedef struct {
+  int32_t n_rec;
+  const int32_t* env_id;     /* [n_rec]        */
+  const int32_t* step;       /* [n_rec]        */
+  const int32_t* version;    /* [n_rec]        */
+  const float* reward;       /* [n_rec]        */
+  const uint8_t* done;       /* [n_rec]        */
+  const float* value;        /* [n_rec]        */
+  const int32_t* tokens;     /* [n_rec*a_tok]  */
+  const float* logp_behav;   /* [n_rec*a_tok]  */
+} rlvla_step_batch;
+
+/* S1 — scatter M records into the buffer.
+ * Semantics = sequential replay in submission order (reading R6), reproduced
+ * bit-exactly for any thread order: record i gets key_i = (version_i << 40) |
+ * (seq_base + i);
+ *   env_id/step out of range        -> counters[OOB] += 1
+ *   version < 0 or > cur_version     -> counters[BAD_VERSION] += 1
+ *   slot already filled              -> counters[DUP] += 1, and the slot takes the whole
+ *                                       record iff key_i > its key
+ *   else                             -> slot written, counters[WRITTEN] += 1
+ * Payloads are copied bit for bit. `seq_base` >= 1 is caller-monotone across calls
+ * (seq_base + n_rec < 2^40); 0 <= cur_version < 2^23. counters: device int64[4], ADDED to.
+ * Returns INVALID_ARG on a key-space overflow or NULL pointers (n_rec == 0 is a no-op). */
+RLVLA_API rlvla_status rlvla_scatter_steps(const rlvla_traj_buffer* buf, const rlvla_step_batch* rec,
+                                 int32_t cur_version, uint64_t seq_base, int64_t* counters,
+                                 void* stream);
+
+enum { RLVLA_ADV_GAE = 0, RLVLA_ADV_GRPO = 1 };
+
+typedef struct {
+  int32_t mode;              /* RLVLA_ADV_GAE | RLVLA_ADV_GRPO                          */
+  /* GAE (Schulman et al. 2016; paper-silent): */
+  float gamma, lam;          /* discount and GAE lambda                                 */
+  int32_t whiten;            /* 1 => adv = (A - mu) / (sigma + whiten_eps), mu/sigma over */
+  float whiten_eps;          /*      all filled steps of ALL ranks (unbiased, R9)          */
+  /* GRPO (Shao et al. 2024): R_e = sum_t r_t over filled steps; A_e = (R_e - mu_g) /   */
+  /* (sigma_g + grpo_eps) over the env's group g, members in ascending global env id.   */
+  const int32_t* group_id;   /* device int32[n_env_global] group of each GLOBAL env, or  */
+                             /* NULL => contiguous groups of group_size                 */
+  int32_t group_size;
+  int32_t std_unbiased;      /* 1 => sigma with n-1 (R10), 0 => population (n)          */
+  float grpo_eps;
+  int32_t env_offset;        /* global id of this rank's env 0 (= rank * n_env)          */
+  int32_t n_env_global;      /* n_env * nranks                                           */
+  /* token bookkeeping for the loss normaliser (slot RLVLA_STAT_N_TOK): */
+  int32_t cur_version, max_staleness;
+} rlvla_adv_params;
+
+/* S2 — advantages for every slot of `buf`.
+ * adv, ret: device float[n_env*t_steps]. GAE: adv = A_t (whitened if p->whiten),
+ * ret = A_t + V_t (raw); GRPO: adv = A_e on filled steps, ret = R_e (ret may be NULL).
+ * Never-filled slots get adv = ret = 0 and cut the GAE recursion (R8).
+ * GAE per env, t = T-1..0: nt_t = v_t (1 - done_t) v_{t+1} (v_T := 1);
+ * delta_t = v_t (r_t + gamma nt_t V_{t+1} - V_t) with V_T = last_value[e] (NULL => 0);
+ * A_t = delta_t + gamma lam nt_t A_{t+1}. Computed as a warp-parallel suffix scan of the
+ * affine maps A -> delta_t + c_t A (fp32, fp64 statistics).
+ * stats: device double[16]; slots 0..5 written and allreduced over `comm` (C1). With
+ * GRPO and comm != NULL the per-env returns are allgathered (C2) first. */
+RLVLA_API rlvla_status rlvla_advantages(const rlvla_traj_buffer* buf, const float* last_value,
+                              const rlvla_adv_params* p, float* adv, float* ret,
+                              double* stats, void* workspace, size_t ws_bytes,
+                              rlvla_comm comm, void* stream);
+
+/* Logit rows: rows x vocab, row r at ptr + r*ld elements. ptr 16-byte aligned for the
+ * vectorised paths (any alignment works on the generic path). */
+typedef struct {
+  const void* ptr;
+  int32_t dtype;   /* rlvla_dtype */
+  int64_t rows;
+  int32_t vocab;   /* V: the softmax normalises over these V columns (reading R3) */
+  int64_t ld;      /* >= vocab, in elements */
+} rlvla_logits;
+
+/* PPO / decoupled-PPO arguments (S4). Row r belongs to decision step s = r / a_tok;
+ * for a micro-batch, offset every per-row pointer by r0 and every per-step pointer by
+ * r0 / a_tok (r0 a multiple of a_tok).
+ *   lag = cur_version - version[s];  m_r = [slot_key[s] != 0] [target ok, finite logp]
+ *                                          [0 <= lag <= max_staleness]
+ *   standard : rho = exp(logp - logp_behav), w = 1
+ *   decoupled: w = min(exp(logp_prox - logp_behav), is_cap) (detached, is_cap <= 0 =>
+ *              no cap), rho = exp(logp - logp_prox)            (AReaL, cited P:18)
+ *   L_r = -w min(rho A_s, clip(rho, 1 - eps_low, 1 + eps_high) A_s);  Loss = sum m L / N
+ *   dLoss/dlogp_r = -m_r w A_s rho [active] / N, ties at the clip bound active (R11). */
+typedef struct {
+  const float* logp_behav;    /* [rows]                                               */
+  const float* logp_prox;     /* [rows] or NULL => standard PPO                        */
+  const float* adv;           /* [rows / a_tok] per decision step                      */
+  const int32_t* version;     /* [rows / a_tok]                                        */
+  const uint64_t* slot_key;   /* [rows / a_tok] 0 => step never filled (masked)        */
+  int32_t a_tok, cur_version, max_staleness;
+  float eps_low, eps_high, is_cap;
+  double tok_denominator;     /* > 0: N. <= 0: N = adv_stats[RLVLA_STAT_N_TOK] (global, */
+  const double* adv_stats;    /*  device, from rlvla_advantages)                       */
+  float* out_grad_logp;       /* [rows] optional: dLoss/dlogp_r                        */
+  float* out_loss_tok;        /* [rows] optional: m_r L_r (unnormalised)               */
+} rlvla_ppo_args;
+
+/* S3 (+S4) — action-token log-probs over logit rows (P:39 action tokens; P:88 actor
+ * micro-batch forward/backward):
+ *   lse_r = m + ln sum_j exp(x_rj - m);  logp_r = x_{r,a_r} - lse_r;
+ *   H_r = lse_r - sum_j p_rj x_rj;       dx_rj = g_r (1[j = a_r] - exp(x_rj - lse_r)).
+ * Modes:
+ *   forward only    : fused == NULL, grad_logp == NULL, dlogits == NULL
+ *   external bwd    : fused == NULL, grad_logp != NULL, lse (input!) != NULL, dlogits;
+ *                     one read of x, one write of dlogits, logp not written
+ *   fused PPO       : fused != NULL: one pass computing logp, the PPO epilogue g_r and
+ *                     (if dlogits != NULL) dlogits; stats slots 6..15; over `comm` C3.
+ * target: int32[rows]; -1 => ignore (logp = 0, zero gradient row); other targets
+ * outside [0, V) are counted in N_BAD_TOK and treated as ignored (R4). Non-finite
+ * results (NaN/+inf logits, all -inf row, -inf target logit) give a non-finite logp,
+ * are counted and masked (R5). logp: float[rows] (written except in external bwd);
+ * lse: float[rows] or NULL (output in forward/fused modes). dlogits: same dtype/ld as
+ * x, may alias x->ptr (each row is read completely before it is written); masked rows
+ * are written as zeros. stats: NULL or device double[16]. */
+RLVLA_API rlvla_status rlvla_logprob_fwd_bwd(const rlvla_logits* x, const int32_t* target, float* logp,
+                                   float* lse, const float* grad_logp,
+                                   const rlvla_ppo_args* fused, void* dlogits, double* stats,
+                                   void* workspace, size_t ws_bytes, rlvla_comm comm,
+                                   void* stream);
+
+/* S4 — the same surrogate over precomputed log-probs logp[rows] (e.g. produced by
+ * another forward). target: int32[rows] or NULL (all usable); rows whose target is
+ * outside [0, ...) or whose logp is non-finite are masked (no vocab bound is known
+ * here, so only target < 0 / non-finite are checked). grad_logp: float[rows] output
+ * (required); loss_tok: float[rows] or NULL. stats slots 6..15 (entropy slot = 0). */
+RLVLA_API rlvla_status rlvla_ppo_loss(const float* logp, int64_t rows, const int32_t* target,
+                            const rlvla_ppo_args* a, float* grad_logp, float* loss_tok,
+                            double* stats, void* workspace, size_t ws_bytes, rlvla_comm comm,
+                            void* stream);
+
+/* Workspace bytes for calls on buffers/logits up to these sizes (host-only, no GPU). */
+RLVLA_API size_t rlvla_workspace_bytes(int64_t rows, int32_t n_env_global, int32_t t_steps);
+
+/* Communicator over NCCL (NVLink/NVSwitch). Rank 0 calls rlvla_comm_unique_id and the
+ * 128 bytes are broadcast by the caller (e.g. torch.distributed). Host pointers. */
+RLVLA_API rlvla_status rlvla_comm_unique_id(void* out_id_128_bytes);
+RLVLA_API rlvla_status rlvla_comm_init(const void* nccl_unique_id, int32_t nranks, int32_t rank,
+                             rlvla_comm* out);
+RLVLA_API rlvla_status rlvla_comm_destroy(rlvla_comm c);
+
+RLVLA_API const char* rlvla_status_string(rlvla_status s);
+RLVLA_API int32_t rlvla_abi_version(void);
+/* Version of the NCCL library actually loaded (e.g. 22809), 0 if unavailable. */
+RLVLA_API int32_t rlvla_nccl_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RLVLA_H_ */

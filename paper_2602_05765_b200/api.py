@@ -1,0 +1,230 @@
+"""Thin Python binding of the C ABI (include/rlvla.h), same names as the C entry points.
+
+Argument marshalling only: torch tensors (device memory the caller owns) are turned into
+raw pointers, the current CUDA stream is passed through, and a non-OK status raises.
+Every step of the path runs in librlvla.so's kernels; nothing here computes.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _abi as A
+from ._abi import lib
+
+
+class RlvlaError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = lib().rlvla_status_string(status).decode()
+        super().__init__(f"{where}: status {status} ({msg})")
+        self.status = status
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"expected a torch.Tensor, got {type(t)}")
+    return t.data_ptr()
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        if not torch.cuda.is_available():
+            return None
+        stream = torch.cuda.current_stream()
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def _check(st: int, where: str, check: bool) -> int:
+    if check and st != A.OK:
+        raise RlvlaError(st, where)
+    return st
+
+
+# --------------------------------------------------------------------------------------
+# containers (device memory owned by the caller; allocation is plumbing)
+# --------------------------------------------------------------------------------------
+@dataclass
+class TrajectoryBuffer:
+    """rlvla_traj_buffer: one rank's shard, [n_env, t_steps] steps x a_tok tokens."""
+    n_env: int
+    t_steps: int
+    a_tok: int
+    slot_key: torch.Tensor     # int64 view of uint64 [E, T]
+    reward: torch.Tensor       # f32 [E, T]
+    done: torch.Tensor         # u8 [E, T]
+    value: torch.Tensor        # f32 [E, T]
+    version: torch.Tensor      # i32 [E, T]
+    tokens: torch.Tensor       # i32 [E, T, A]
+    logp_behav: torch.Tensor   # f32 [E, T, A]
+
+    @classmethod
+    def allocate(cls, n_env, t_steps, a_tok, device="cuda"):
+        z = lambda *s, dt: torch.zeros(*s, dtype=dt, device=device)  # noqa: E731
+        return cls(n_env, t_steps, a_tok, z(n_env, t_steps, dt=torch.int64),
+                   z(n_env, t_steps, dt=torch.float32), z(n_env, t_steps, dt=torch.uint8),
+                   z(n_env, t_steps, dt=torch.float32), z(n_env, t_steps, dt=torch.int32),
+                   z(n_env, t_steps, a_tok, dt=torch.int32),
+                   z(n_env, t_steps, a_tok, dt=torch.float32))
+
+    def reset(self):
+        self.slot_key.zero_()
+
+    def c(self) -> A.c_traj_buffer:
+        return A.c_traj_buffer(self.n_env, self.t_steps, self.a_tok, _ptr(self.slot_key),
+                               _ptr(self.reward), _ptr(self.done), _ptr(self.value),
+                               _ptr(self.version), _ptr(self.tokens), _ptr(self.logp_behav))
+
+
+@dataclass
+class StepBatch:
+    """rlvla_step_batch: M records in arrival order (device tensors)."""
+    env_id: torch.Tensor      # i32 [M]
+    step: torch.Tensor        # i32 [M]
+    version: torch.Tensor     # i32 [M]
+    reward: torch.Tensor      # f32 [M]
+    done: torch.Tensor        # u8 [M]
+    value: torch.Tensor       # f32 [M]
+    tokens: torch.Tensor      # i32 [M, A]
+    logp_behav: torch.Tensor  # f32 [M, A]
+
+    @property
+    def n(self) -> int:
+        return int(self.env_id.shape[0])
+
+    def slice(self, sl: slice) -> "StepBatch":
+        return StepBatch(*(getattr(self, f)[sl] for f in
+                           ("env_id", "step", "version", "reward", "done", "value", "tokens",
+                            "logp_behav")))
+
+    def c(self) -> A.c_step_batch:
+        return A.c_step_batch(self.n, _ptr(self.env_id), _ptr(self.step), _ptr(self.version),
+                              _ptr(self.reward), _ptr(self.done), _ptr(self.value),
+                              _ptr(self.tokens), _ptr(self.logp_behav))
+
+
+def workspace(n_env_global: int = 1, rows: int = 0, t_steps: int = 0, device="cuda"):
+    """Zero-filled, 256-byte aligned workspace of rlvla_workspace_bytes(...) bytes."""
+    nb = int(lib().rlvla_workspace_bytes(rows, n_env_global, t_steps))
+    return torch.zeros(nb + 256, dtype=torch.uint8, device=device)
+
+
+def _ws_ptr(ws):
+    if ws is None:
+        return None, 0
+    p = ws.data_ptr()
+    off = (-p) % 256
+    return p + off, ws.numel() - off
+
+
+# --------------------------------------------------------------------------------------
+# entry points
+# --------------------------------------------------------------------------------------
+def rlvla_scatter_steps(buf: TrajectoryBuffer, rec: StepBatch, cur_version: int,
+                        seq_base: int, counters: torch.Tensor, stream=None, check=True) -> int:
+    b, r = buf.c(), rec.c()
+    st = lib().rlvla_scatter_steps(ctypes.byref(b), ctypes.byref(r), cur_version, seq_base,
+                                   _ptr(counters), _stream(stream))
+    return _check(st, "rlvla_scatter_steps", check)
+
+
+def adv_params(mode, *, gamma=0.99, lam=0.95, whiten=False, whiten_eps=1e-8, group_id=None,
+               group_size=0, std_unbiased=True, grpo_eps=1e-6, env_offset=0, n_env_global=0,
+               cur_version=0, max_staleness=1) -> A.c_adv_params:
+    return A.c_adv_params(A.ADV_GAE if mode == "gae" else A.ADV_GRPO, gamma, lam, int(whiten),
+                          whiten_eps, _ptr(group_id), group_size, int(std_unbiased), grpo_eps,
+                          env_offset, n_env_global, cur_version, max_staleness)
+
+
+def rlvla_advantages(buf: TrajectoryBuffer, last_value, params: A.c_adv_params, adv, ret,
+                     stats, ws, comm=None, stream=None, check=True) -> int:
+    b = buf.c()
+    wp, wn = _ws_ptr(ws)
+    st = lib().rlvla_advantages(ctypes.byref(b), _ptr(last_value), ctypes.byref(params),
+                                _ptr(adv), _ptr(ret), _ptr(stats), wp, wn,
+                                comm.handle if comm is not None else None, _stream(stream))
+    return _check(st, "rlvla_advantages", check)
+
+
+def logits_desc(x: torch.Tensor, vocab: int | None = None) -> A.c_logits:
+    if x.dim() != 2 or x.stride(1) != 1:
+        raise ValueError("logits must be a 2-D row-major tensor")
+    dt = {torch.float32: A.F32, torch.bfloat16: A.BF16}[x.dtype]
+    return A.c_logits(_ptr(x), dt, x.shape[0], vocab or x.shape[1], x.stride(0))
+
+
+def ppo_args(*, logp_behav, adv, version, slot_key, a_tok, cur_version, max_staleness=1,
+             eps_low=0.2, eps_high=0.2, is_cap=0.0, logp_prox=None, tok_denominator=0.0,
+             adv_stats=None, out_grad_logp=None, out_loss_tok=None) -> A.c_ppo_args:
+    return A.c_ppo_args(_ptr(logp_behav), _ptr(logp_prox), _ptr(adv), _ptr(version),
+                        _ptr(slot_key), a_tok, cur_version, max_staleness, eps_low, eps_high,
+                        is_cap, tok_denominator, _ptr(adv_stats), _ptr(out_grad_logp),
+                        _ptr(out_loss_tok))
+
+
+def rlvla_logprob_fwd_bwd(x: torch.Tensor, target, logp=None, lse=None, grad_logp=None,
+                          fused: A.c_ppo_args | None = None, dlogits=None, stats=None, ws=None,
+                          comm=None, stream=None, vocab=None, check=True) -> int:
+    xd = logits_desc(x, vocab)
+    wp, wn = _ws_ptr(ws)
+    st = lib().rlvla_logprob_fwd_bwd(ctypes.byref(xd), _ptr(target), _ptr(logp), _ptr(lse),
+                                     _ptr(grad_logp),
+                                     ctypes.byref(fused) if fused is not None else None,
+                                     _ptr(dlogits), _ptr(stats), wp, wn,
+                                     comm.handle if comm is not None else None, _stream(stream))
+    return _check(st, "rlvla_logprob_fwd_bwd", check)
+
+
+def rlvla_ppo_loss(logp, target, args: A.c_ppo_args, grad_logp, loss_tok=None, stats=None,
+                   ws=None, comm=None, stream=None, check=True) -> int:
+    wp, wn = _ws_ptr(ws)
+    st = lib().rlvla_ppo_loss(_ptr(logp), logp.numel(), _ptr(target), ctypes.byref(args),
+                              _ptr(grad_logp), _ptr(loss_tok), _ptr(stats), wp, wn,
+                              comm.handle if comm is not None else None, _stream(stream))
+    return _check(st, "rlvla_ppo_loss", check)
+
+
+def rlvla_workspace_bytes(rows: int, n_env_global: int, t_steps: int) -> int:
+    return int(lib().rlvla_workspace_bytes(rows, n_env_global, t_steps))
+
+
+def rlvla_abi_version() -> int:
+    return int(lib().rlvla_abi_version())
+
+
+def rlvla_nccl_version() -> int:
+    return int(lib().rlvla_nccl_version())
+
+
+class Comm:
+    """rlvla_comm over NCCL; the 128-byte unique id travels over a torch ProcessGroup."""
+
+    def __init__(self, handle, nranks, rank):
+        self.handle, self.nranks, self.rank = handle, nranks, rank
+
+    @classmethod
+    def from_process_group(cls, group=None, device=None):
+        import torch.distributed as dist
+        rank, n = dist.get_rank(group), dist.get_world_size(group)
+        uid = (ctypes.c_ubyte * 128)()
+        if rank == 0:
+            _check(lib().rlvla_comm_unique_id(uid), "rlvla_comm_unique_id", True)
+        backend = dist.get_backend(group)
+        dev = device if (backend == "nccl") else "cpu"
+        t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device=dev)
+        dist.broadcast(t, src=0, group=group)
+        raw = bytes(t.cpu().tolist())
+        uid2 = (ctypes.c_ubyte * 128).from_buffer_copy(raw)
+        h = ctypes.c_void_p()
+        _check(lib().rlvla_comm_init(uid2, n, rank, ctypes.byref(h)), "rlvla_comm_init", True)
+        return cls(h, n, rank)
+
+    def destroy(self):
+        if self.handle:
+            lib().rlvla_comm_destroy(self.handle)
+            self.handle = None

@@ -1,0 +1,307 @@
+// api.cu — the extern "C" boundary (include/rlvla.h): argument validation, dispatch to the
+// kernels, and the NCCL collectives C1 (advantage statistics allreduce), C2 (GRPO returns
+// allgather) and C3 (loss statistics allreduce), all enqueued on the caller's stream.
+#include <nccl.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "internal.cuh"
+
+struct rlvla_comm_s {
+  ncclComm_t comm;
+  int nranks;
+  int rank;
+};
+
+namespace rlvla {
+
+const DeviceInfo& device_info() {
+  static std::mutex mu;
+  static DeviceInfo cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    static DeviceInfo none;
+    return none;
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  DeviceInfo& d = cache[dev];
+  if (d.device != dev) {
+    cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    d.device = dev;
+  }
+  return d;
+}
+
+bool sync_check_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("RLVLA_SYNC_CHECK");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+}  // namespace rlvla
+
+using namespace rlvla;
+
+namespace {
+
+constexpr size_t kAlignWs = 256;
+
+size_t ws_bytes_for(int32_t n_env_global) {
+  const size_t r = (size_t(n_env_global > 0 ? n_env_global : 1) * sizeof(float) + kAlignWs - 1) /
+                   kAlignWs * kAlignWs;
+  return kCtrlBytes + kPartialBytes + r;
+}
+
+rlvla_status cuda_status(cudaError_t e) { return e == cudaSuccess ? RLVLA_OK : RLVLA_ERR_CUDA; }
+
+bool device_ready() { return device_info().sm_count > 0; }
+
+rlvla_status check_buffer(const rlvla_traj_buffer* b) {
+  if (!b) return RLVLA_ERR_INVALID_ARG;
+  if (b->n_env <= 0 || b->t_steps <= 0 || b->a_tok <= 0) return RLVLA_ERR_INVALID_ARG;
+  if (!b->slot_key || !b->reward || !b->done || !b->value || !b->version || !b->tokens ||
+      !b->logp_behav)
+    return RLVLA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(b->slot_key) % 8) return RLVLA_ERR_INVALID_ARG;
+  return RLVLA_OK;
+}
+
+rlvla_status check_ppo_args(const rlvla_ppo_args* f) {
+  if (!f->logp_behav || !f->adv || !f->version || !f->slot_key) return RLVLA_ERR_INVALID_ARG;
+  if (f->a_tok <= 0 || f->max_staleness < 0) return RLVLA_ERR_INVALID_ARG;
+  if (!(f->eps_low >= 0.f) || !(f->eps_high >= 0.f) || f->eps_low >= 1.f) return RLVLA_ERR_INVALID_ARG;
+  if (!(f->tok_denominator > 0.0) && !f->adv_stats) return RLVLA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(f->slot_key) % 8) return RLVLA_ERR_INVALID_ARG;
+  return RLVLA_OK;
+}
+
+rlvla_status allreduce_stats(double* p, int n, rlvla_comm c, cudaStream_t s) {
+  if (!c || c->nranks <= 1) return RLVLA_OK;
+  return ncclAllReduce(p, p, size_t(n), ncclDouble, ncclSum, c->comm, s) == ncclSuccess
+             ? RLVLA_OK
+             : RLVLA_ERR_NCCL;
+}
+
+rlvla_status sync_check_stats(const double* stats, int slot, cudaStream_t s) {
+  if (!sync_check_enabled() || !stats) return RLVLA_OK;
+  double v = 0;
+  if (cudaMemcpyAsync(&v, stats + slot, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return RLVLA_ERR_CUDA;
+  return v != 0.0 ? RLVLA_ERR_DATA : RLVLA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+RLVLA_API int32_t rlvla_abi_version(void) { return RLVLA_ABI_VERSION; }
+
+RLVLA_API const char* rlvla_status_string(rlvla_status s) {
+  switch (s) {
+    case RLVLA_OK: return "ok";
+    case RLVLA_ERR_INVALID_ARG: return "invalid argument";
+    case RLVLA_ERR_UNSUPPORTED: return "unsupported configuration";
+    case RLVLA_ERR_CUDA: return "CUDA error";
+    case RLVLA_ERR_NCCL: return "NCCL error";
+    case RLVLA_ERR_DATA: return "data error counted on device (RLVLA_SYNC_CHECK)";
+    default: return "unknown status";
+  }
+}
+
+RLVLA_API int32_t rlvla_nccl_version(void) {
+  int v = 0;
+  if (ncclGetVersion(&v) != ncclSuccess) return 0;
+  return v;
+}
+
+RLVLA_API size_t rlvla_workspace_bytes(int64_t rows, int32_t n_env_global, int32_t t_steps) {
+  (void)rows;
+  (void)t_steps;
+  return ws_bytes_for(n_env_global);
+}
+
+RLVLA_API rlvla_status rlvla_scatter_steps(const rlvla_traj_buffer* buf,
+                                           const rlvla_step_batch* rec, int32_t cur_version,
+                                           uint64_t seq_base, int64_t* counters, void* stream) {
+  rlvla_status st = check_buffer(buf);
+  if (st != RLVLA_OK) return st;
+  if (!rec || rec->n_rec < 0 || !counters) return RLVLA_ERR_INVALID_ARG;
+  if (cur_version < 0 || cur_version >= (1 << 23)) return RLVLA_ERR_INVALID_ARG;
+  if (seq_base < 1 || seq_base + uint64_t(rec->n_rec) >= (uint64_t(1) << 40)) return RLVLA_ERR_INVALID_ARG;
+  if (rec->n_rec == 0) return RLVLA_OK;
+  if (!rec->env_id || !rec->step || !rec->version || !rec->reward || !rec->done || !rec->value ||
+      !rec->tokens || !rec->logp_behav)
+    return RLVLA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(counters) % 8) return RLVLA_ERR_INVALID_ARG;
+  if (!device_ready()) return RLVLA_ERR_CUDA;
+  ScatterArgs a{*buf, *rec, cur_version, seq_base, counters};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  st = cuda_status(launch_scatter(a, s));
+  if (st != RLVLA_OK || !sync_check_enabled()) return st;
+  int64_t c[4];
+  if (cudaMemcpyAsync(c, counters, sizeof(c), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return RLVLA_ERR_CUDA;
+  return (c[RLVLA_CNT_OOB] || c[RLVLA_CNT_BAD_VERSION]) ? RLVLA_ERR_DATA : RLVLA_OK;
+}
+
+RLVLA_API rlvla_status rlvla_advantages(const rlvla_traj_buffer* buf, const float* last_value,
+                                        const rlvla_adv_params* p, float* adv, float* ret,
+                                        double* stats, void* workspace, size_t ws_bytes,
+                                        rlvla_comm comm, void* stream) {
+  rlvla_status st = check_buffer(buf);
+  if (st != RLVLA_OK) return st;
+  if (!p || !adv || !stats || !workspace) return RLVLA_ERR_INVALID_ARG;
+  if (p->mode != RLVLA_ADV_GAE && p->mode != RLVLA_ADV_GRPO) return RLVLA_ERR_INVALID_ARG;
+  if (p->mode == RLVLA_ADV_GAE && !ret) return RLVLA_ERR_INVALID_ARG;
+  if (p->max_staleness < 0) return RLVLA_ERR_INVALID_ARG;
+  const int nranks = comm ? comm->nranks : 1;
+  const int rank = comm ? comm->rank : 0;
+  if (p->n_env_global != buf->n_env * nranks || p->env_offset != rank * buf->n_env)
+    return RLVLA_ERR_INVALID_ARG;
+  if (p->mode == RLVLA_ADV_GRPO && !p->group_id && p->group_size <= 0) return RLVLA_ERR_INVALID_ARG;
+  if (p->mode == RLVLA_ADV_GRPO && !(p->grpo_eps >= 0.f)) return RLVLA_ERR_INVALID_ARG;
+  if (ws_bytes < ws_bytes_for(p->n_env_global)) return RLVLA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(workspace) % kAlignWs || reinterpret_cast<uintptr_t>(stats) % 8)
+    return RLVLA_ERR_INVALID_ARG;
+  if (!device_ready()) return RLVLA_ERR_CUDA;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  AdvArgs a{*buf, last_value, *p, adv, ret, stats, carve(workspace)};
+  st = cuda_status(launch_adv_pass1(a, s));
+  if (st != RLVLA_OK) return st;
+  if (comm && comm->nranks > 1) {
+    if (ncclGroupStart() != ncclSuccess) return RLVLA_ERR_NCCL;
+    ncclResult_t r1 = ncclAllReduce(stats, stats, 6, ncclDouble, ncclSum, comm->comm, s);
+    ncclResult_t r2 = ncclSuccess;
+    if (p->mode == RLVLA_ADV_GRPO) {
+      float* rg = a.ws.r_global;
+      r2 = ncclAllGather(rg + size_t(rank) * buf->n_env, rg, size_t(buf->n_env), ncclFloat,
+                         comm->comm, s);
+    }
+    ncclResult_t r3 = ncclGroupEnd();
+    if (r1 != ncclSuccess || r2 != ncclSuccess || r3 != ncclSuccess) return RLVLA_ERR_NCCL;
+  }
+  st = cuda_status(launch_adv_pass2(a, s));
+  if (st != RLVLA_OK) return st;
+  return sync_check_stats(stats, RLVLA_STAT_N_BAD_STEPS, s);
+}
+
+RLVLA_API rlvla_status rlvla_logprob_fwd_bwd(const rlvla_logits* x, const int32_t* target,
+                                             float* logp, float* lse, const float* grad_logp,
+                                             const rlvla_ppo_args* fused, void* dlogits,
+                                             double* stats, void* workspace, size_t ws_bytes,
+                                             rlvla_comm comm, void* stream) {
+  if (!x || !x->ptr || !target) return RLVLA_ERR_INVALID_ARG;
+  if (x->dtype != RLVLA_F32 && x->dtype != RLVLA_BF16) return RLVLA_ERR_INVALID_ARG;
+  if (x->rows < 0 || x->vocab < 1 || x->ld < x->vocab) return RLVLA_ERR_INVALID_ARG;
+  if (fused && grad_logp) return RLVLA_ERR_INVALID_ARG;
+  if (grad_logp) {
+    if (!lse || !dlogits) return RLVLA_ERR_INVALID_ARG;
+  } else if (!logp) {
+    return RLVLA_ERR_INVALID_ARG;
+  }
+  if (fused) {
+    rlvla_status st = check_ppo_args(fused);
+    if (st != RLVLA_OK) return st;
+    if (x->rows % fused->a_tok) return RLVLA_ERR_INVALID_ARG;
+  }
+  if (stats && !grad_logp) {
+    if (!workspace || ws_bytes < ws_bytes_for(1) || reinterpret_cast<uintptr_t>(workspace) % kAlignWs)
+      return RLVLA_ERR_INVALID_ARG;
+  }
+  if (x->rows == 0) return RLVLA_OK;
+  if (!device_ready()) return RLVLA_ERR_CUDA;
+  LpArgs a{};
+  a.x = *x;
+  a.target = target;
+  a.logp = logp;
+  a.lse = lse;
+  a.grad_logp = grad_logp;
+  a.fused = fused != nullptr;
+  if (fused) a.f = *fused;
+  a.dlogits = dlogits;
+  a.stats = grad_logp ? nullptr : stats;
+  if (workspace) a.ws = carve(workspace);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  rlvla_status st = cuda_status(launch_logprob(a, s));
+  if (st != RLVLA_OK) return st;
+  if (a.stats) {
+    st = allreduce_stats(stats + RLVLA_STAT_LOSS, RLVLA_STAT_DENOM - RLVLA_STAT_LOSS, comm, s);
+    if (st != RLVLA_OK) return st;
+    return sync_check_stats(stats, RLVLA_STAT_N_BAD_TOK, s);
+  }
+  return RLVLA_OK;
+}
+
+RLVLA_API rlvla_status rlvla_ppo_loss(const float* logp, int64_t rows, const int32_t* target,
+                                      const rlvla_ppo_args* f, float* grad_logp, float* loss_tok,
+                                      double* stats, void* workspace, size_t ws_bytes,
+                                      rlvla_comm comm, void* stream) {
+  if (!logp || !f || !grad_logp || rows < 0) return RLVLA_ERR_INVALID_ARG;
+  rlvla_status st = check_ppo_args(f);
+  if (st != RLVLA_OK) return st;
+  if (rows % f->a_tok) return RLVLA_ERR_INVALID_ARG;
+  if (stats && (!workspace || ws_bytes < ws_bytes_for(1) ||
+                reinterpret_cast<uintptr_t>(workspace) % kAlignWs))
+    return RLVLA_ERR_INVALID_ARG;
+  if (rows == 0) return RLVLA_OK;
+  if (!device_ready()) return RLVLA_ERR_CUDA;
+  PpoArgs a{};
+  a.logp = logp;
+  a.rows = rows;
+  a.target = target;
+  a.f = *f;
+  a.grad_logp = grad_logp;
+  a.loss_tok = loss_tok;
+  a.stats = stats;
+  if (workspace) a.ws = carve(workspace);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  st = cuda_status(launch_ppo_loss(a, s));
+  if (st != RLVLA_OK) return st;
+  if (stats) {
+    st = allreduce_stats(stats + RLVLA_STAT_LOSS, RLVLA_STAT_DENOM - RLVLA_STAT_LOSS, comm, s);
+    if (st != RLVLA_OK) return st;
+    return sync_check_stats(stats, RLVLA_STAT_N_BAD_TOK, s);
+  }
+  return RLVLA_OK;
+}
+
+RLVLA_API rlvla_status rlvla_comm_unique_id(void* out) {
+  if (!out) return RLVLA_ERR_INVALID_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return RLVLA_ERR_NCCL;
+  std::memcpy(out, &id, sizeof(id));
+  return RLVLA_OK;
+}
+
+RLVLA_API rlvla_status rlvla_comm_init(const void* id, int32_t nranks, int32_t rank,
+                                       rlvla_comm* out) {
+  if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks) return RLVLA_ERR_INVALID_ARG;
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  rlvla_comm c = new rlvla_comm_s{};
+  c->nranks = nranks;
+  c->rank = rank;
+  if (ncclCommInitRank(&c->comm, nranks, uid, rank) != ncclSuccess) {
+    delete c;
+    return RLVLA_ERR_NCCL;
+  }
+  *out = c;
+  return RLVLA_OK;
+}
+
+RLVLA_API rlvla_status rlvla_comm_destroy(rlvla_comm c) {
+  if (!c) return RLVLA_OK;
+  ncclResult_t r = ncclCommDestroy(c->comm);
+  delete c;
+  return r == ncclSuccess ? RLVLA_OK : RLVLA_ERR_NCCL;
+}
+
+}  // extern "C"

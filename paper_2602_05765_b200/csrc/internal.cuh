@@ -1,0 +1,248 @@
+// internal.cuh — device helpers and launch declarations shared by the librlvla kernels.
+// Nothing here is shared with oracle/ (the CPU reference is numpy).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "rlvla.h"
+
+namespace rlvla {
+
+constexpr int kMaxPartialBlocks = 2048;          // per-CTA fp64 partial rows in workspace
+constexpr size_t kCtrlBytes = 256;               // control words (last-block counters)
+constexpr size_t kPartialBytes = size_t(kMaxPartialBlocks) * RLVLA_NSTATS * sizeof(double);
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+// control-word indices (uint32 each) inside the workspace header
+enum { CTRL_SCATTER = 0, CTRL_ADV = 1, CTRL_LOGPROB = 2, CTRL_PPO = 3, CTRL_ADV2 = 4 };
+
+struct Workspace {
+  unsigned* ctrl;      // [64]
+  double* partials;    // [kMaxPartialBlocks][16]
+  float* r_global;     // [n_env_global] (GRPO returns)
+};
+
+inline Workspace carve(void* ws) {
+  Workspace w;
+  uint8_t* b = static_cast<uint8_t*>(ws);
+  w.ctrl = reinterpret_cast<unsigned*>(b);
+  w.partials = reinterpret_cast<double*>(b + kCtrlBytes);
+  w.r_global = reinterpret_cast<float*>(b + kCtrlBytes + kPartialBytes);
+  return w;
+}
+
+// ------------------------------------------------------------------------------------
+// device helpers
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// 2^x on the MUFU (ex2.approx.ftz.f32): one SFU op per call.
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// bf16 pair (one 32-bit word) -> two fp32, exact (bf16 = top half of fp32)
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+// two fp32 -> bf16x2 word, round to nearest even (cvt.rn.bf16x2.f32)
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// packed bf16x2 max (one HMNMX2 per pair); NaN inputs are dropped here and propagate
+// through the exponent sums instead (reading R5).
+__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
+  __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&a);
+  __nv_bfloat162 y = *reinterpret_cast<__nv_bfloat162*>(&b);
+  __nv_bfloat162 z = __hmax2(x, y);
+  return *reinterpret_cast<uint32_t*>(&z);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// mbarrier / bulk-async-copy (TMA engine) wrappers, sm_90+ PTX (SASS: SYNCS.*, UBLKCP)
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// try_wait suspends in hardware for a bounded time per call; ~2^26 failed calls (many
+// seconds) means a lost transaction: trap instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t n = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if (++n > (1u << 26)) __trap();
+  }
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// 1-D bulk copy global -> shared, completion counted on `bar` in bytes
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+// small async copies (LDGSTS) whose completion arrives on an mbarrier (noinc)
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stg_stream(uint4* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// Last-block-done finalize: each CTA has written partials[blockIdx.x][0..nslot); the
+// last CTA to arrive sums them in fixed CTA order (deterministic, no float atomics) and
+// returns true in every thread of that CTA. Caller uses `out` (per-slot total) then.
+__device__ __forceinline__ bool last_block_reduce(unsigned* ctrl_word, const double* partials,
+                                                  int nslot, double* out_smem) {
+  __shared__ bool am_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned prev = atomicAdd(ctrl_word, 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return false;
+  __threadfence();
+  for (int s = threadIdx.x; s < nslot; s += blockDim.x) {
+    double acc = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) acc += __ldcg(partials + size_t(b) * RLVLA_NSTATS + s);
+    out_smem[s] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *ctrl_word = 0u;  // leave the workspace reusable
+  return true;
+}
+
+// ------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------
+struct DeviceInfo {
+  int device = -1;
+  int sm_count = 0;
+  int smem_optin = 0;
+};
+const DeviceInfo& device_info();          // cached per device (thread-safe)
+bool sync_check_enabled();
+
+// launches (return cudaError_t of the launch)
+struct ScatterArgs {
+  rlvla_traj_buffer buf;
+  rlvla_step_batch rec;
+  int32_t cur_version;
+  uint64_t seq_base;
+  int64_t* counters;
+};
+cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s);
+
+struct AdvArgs {
+  rlvla_traj_buffer buf;
+  const float* last_value;
+  rlvla_adv_params p;
+  float* adv;
+  float* ret;
+  double* stats;
+  Workspace ws;
+};
+cudaError_t launch_adv_pass1(const AdvArgs& a, cudaStream_t s);   // GAE scan | GRPO returns
+cudaError_t launch_adv_pass2(const AdvArgs& a, cudaStream_t s);   // whiten | GRPO normalise
+
+struct LpArgs {
+  rlvla_logits x;
+  const int32_t* target;
+  float* logp;
+  float* lse;
+  const float* grad_logp;
+  bool fused;
+  rlvla_ppo_args f;
+  void* dlogits;
+  double* stats;
+  Workspace ws;
+};
+enum LpPath { LP_PATH_TMA = 0, LP_PATH_WARP = 1, LP_PATH_GENERIC = 2 };
+LpPath select_lp_path(const LpArgs& a);
+cudaError_t launch_logprob(const LpArgs& a, cudaStream_t s);
+
+struct PpoArgs {
+  const float* logp;
+  int64_t rows;
+  const int32_t* target;
+  rlvla_ppo_args f;
+  float* grad_logp;
+  float* loss_tok;
+  double* stats;
+  Workspace ws;
+};
+cudaError_t launch_ppo_loss(const PpoArgs& a, cudaStream_t s);
+
+}  // namespace rlvla

@@ -1,0 +1,711 @@
+// logprob.cu — S3 (+S4): action-token log-softmax + gather, forward and backward, fused
+// with the PPO epilogue. The dominant kernel of the path: >= 99.98% of its HBM bytes are
+// one read of the logits and one write of dlogits.
+//
+// Definition (P:39 action tokens; textbook log-softmax, reading R3-R5):
+//   lse = m + ln sum_j e^{x_j - m}, logp = x_a - lse, H = lse - sum_j p_j x_j,
+//   dx_j = g (1[j=a] - p_j).
+//
+// Three kernels, one per size class:
+//   lp_tma_kernel     bf16, 2048 < V <= 32768 (OpenVLA 32000 vocab). Persistent, one
+//                     1024-thread CTA per SM. Rows are staged HBM -> SMEM by the TMA engine
+//                     (cp.async.bulk, 1-D, 64 KB per row, up to 4-stage ring, mbarrier
+//                     completion, L2 evict_first). Each thread owns 4 x 16 B of the row,
+//                     keeps e_j = 2^{(x_j - m_warp) log2e} in registers (ONE ex2 per
+//                     element), one __syncthreads per row combines the 32 warp partials,
+//                     and dlogits leave as 128-bit streaming stores straight from
+//                     registers. The refill of the freed stage is issued right after
+//                     the barrier, so 2-3 rows are in flight per SM.
+//   lp_warp_kernel    V <= 2048 (e.g. the 256-bin tiny config): one warp per row,
+//                     register-resident row via 128-bit loads.
+//   lp_generic_kernel any V / alignment / dtype: one CTA per row, three passes.
+#include "epilogue.cuh"
+
+namespace rlvla {
+namespace {
+
+enum { MODE_FWD = 0, MODE_FUSED = 1, MODE_BWD = 2 };
+
+struct Lp {
+  const void* x;
+  int64_t rows;
+  int V;
+  int64_t ld;
+  const int32_t* target;
+  float* logp;
+  float* lse_out;
+  const float* lse_in;
+  const float* g_in;
+  void* dx;
+  // fused PPO
+  const float* lpb;
+  const float* lpp;
+  const float* adv;
+  const int32_t* ver;
+  const uint64_t* key;
+  int A;
+  PpoConst pc;
+  double N;                  // > 0: explicit N; else read adv_stats[N_TOK] on the device
+  const double* adv_stats;
+  float* out_g;
+  float* out_L;
+  // stats
+  double* stats;
+  double* partials;
+  unsigned* ctrl;
+};
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// status of a row's target and result: 0 usable, 1 ignore, 2 bad target, 3 non-finite
+__device__ __forceinline__ int row_status(int a, int V, float lse, float logp) {
+  if (a == -1) return 1;
+  if (a < 0 || a >= V) return 2;
+  if (!isfinite(lse) || !isfinite(logp)) return 3;
+  return 0;
+}
+
+// Per-row outputs shared by all kernels once (lse, logp, H) are known. Every caller
+// thread gets g; `writer` threads store the per-row outputs and accumulate stats.
+template <int MODE>
+__device__ __forceinline__ float finish_row(const Lp& p, const PpoConst& pc, int64_t r, int a,
+                                            float lse, float logp,
+                                            float H, float lpb, float lpp, float advv, int ver,
+                                            uint64_t key, bool writer, double* acc) {
+  const int st = row_status(a, p.V, lse, logp);
+  float g = 0.f, lt = 0.f;
+  RowStats rs;
+  PpoRowIn in;
+  in.tgt_status = st;
+  in.logp = (st == 1 || st == 2) ? 0.f : logp;
+  in.H = H;
+  if (MODE == MODE_FUSED) {
+    in.lpb = lpb;
+    in.lpp = lpp;
+    in.adv = advv;
+    in.ver = ver;
+    in.valid = key != 0ull;
+    g = ppo_row(pc, in, rs, &lt);
+  } else {
+    fwd_row_stats(in, rs);
+  }
+  if (writer) {
+    p.logp[r] = in.logp;
+    if (p.lse_out) p.lse_out[r] = lse;
+    if (MODE == MODE_FUSED) {
+      if (p.out_g) p.out_g[r] = g;
+      if (p.out_L) p.out_L[r] = lt;
+    }
+    if (acc) acc_stats(acc, rs);
+  }
+  return g;
+}
+
+// N for 1/N and the per-kernel copy of the PPO constants
+template <int MODE>
+__device__ __forceinline__ double resolve_pc(const Lp& p, PpoConst& pc) {
+  pc = p.pc;
+  if (MODE != MODE_FUSED) {
+    pc.invN = 0.f;
+    return 0.0;
+  }
+  const double N = loss_denominator(p.N, p.adv_stats);
+  pc.invN = N > 0.0 ? float(1.0 / N) : 0.f;
+  return N;
+}
+
+// =====================================================================================
+// K6/K5/K7 for bf16 rows up to 32768: TMA-staged persistent kernel
+// =====================================================================================
+constexpr int kCtaThreads = 1024;
+constexpr int kVecPerThread = 4;  // 4 x (8 bf16) per thread -> V <= 32768
+constexpr int kMaxStages = 4;
+
+struct __align__(16) StageMeta {
+  int32_t a;
+  float lpb, lpp, adv;
+  int32_t ver;
+  float lse_in, g_in;
+  int32_t pad;
+  uint64_t key;
+  uint64_t pad2;
+};
+
+template <int MODE>
+__device__ __forceinline__ void issue_row(const Lp& p, int64_t r, uint8_t* dst, StageMeta* m,
+                                          uint64_t* bar, uint32_t row_bytes, uint64_t pol) {
+  cp_async4(&m->a, p.target + r);
+  if (MODE == MODE_FUSED) {
+    const int64_t s = r / p.A;
+    cp_async4(&m->lpb, p.lpb + r);
+    if (p.lpp) cp_async4(&m->lpp, p.lpp + r);
+    cp_async4(&m->adv, p.adv + s);
+    cp_async4(&m->ver, p.ver + s);
+    cp_async8(&m->key, p.key + s);
+  } else if (MODE == MODE_BWD) {
+    cp_async4(&m->lse_in, p.lse_in + r);
+    cp_async4(&m->g_in, p.g_in + r);
+  }
+  cp_async_arrive_noinc(bar);
+  mbar_arrive_expect_tx(bar, row_bytes);
+  bulk_g2s(dst, static_cast<const __nv_bfloat16*>(p.x) + r * p.ld, row_bytes, bar, pol);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kCtaThreads, 1)
+    lp_tma_kernel(Lp p, int nstages, uint32_t stage_bytes) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* rowbuf = smem;
+  StageMeta* meta = reinterpret_cast<StageMeta*>(smem + size_t(nstages) * stage_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(meta + kMaxStages);
+  float4* red = reinterpret_cast<float4*>(full + kMaxStages);  // [2][32]
+  double* sacc = reinterpret_cast<double*>(red + 64);           // [16]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int V = p.V;
+  const int nvec = V >> 3;
+  const uint32_t row_bytes = uint32_t(V) * 2u;
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  const int64_t nrow = p.rows > first ? (p.rows - first + stride - 1) / stride : 0;
+  const bool want_stats = p.stats != nullptr && MODE != MODE_BWD;
+  const float L2E = kLog2e;
+  PpoConst pc;
+  const double Nden = resolve_pc<MODE>(p, pc);
+
+  if (tid == 0) {
+    for (int s = 0; s < nstages; ++s) mbar_init(&full[s], 2);
+    fence_mbar_init();
+  }
+  if (tid < 16) sacc[tid] = 0.0;
+  __syncthreads();
+  uint64_t pol = 0;
+  if (tid == 0) {
+    pol = policy_evict_first();
+    const int64_t pre = nrow < nstages ? nrow : nstages;
+    for (int64_t k = 0; k < pre; ++k)
+      issue_row<MODE>(p, first + k * stride, rowbuf + k * stage_bytes, &meta[k], &full[k],
+                      row_bytes, pol);
+  }
+
+  for (int64_t k = 0; k < nrow; ++k) {
+    const int st = int(k % nstages);
+    const uint32_t ph = uint32_t((k / nstages) & 1);
+    const int64_t r = first + k * stride;
+    mbar_wait(&full[st], ph);
+    const uint8_t* row = rowbuf + size_t(st) * stage_bytes;
+    const uint4* rv = reinterpret_cast<const uint4*>(row);
+    const StageMeta* mt = &meta[st];
+    const int a = mt->a;
+    float lpb = 0.f, lpp = 0.f, advv = 0.f, lse_in = 0.f, g_in = 0.f;
+    int ver = 0;
+    uint64_t key = 1;
+    if (MODE == MODE_FUSED) {
+      lpb = mt->lpb;
+      if (p.lpp) lpp = mt->lpp;
+      advv = mt->adv;
+      ver = mt->ver;
+      key = mt->key;
+    } else if (MODE == MODE_BWD) {
+      lse_in = mt->lse_in;
+      g_in = mt->g_in;
+    }
+    const bool tgt_ok = unsigned(a) < unsigned(V);
+    const float xa = tgt_ok ? bf_lo(uint32_t(reinterpret_cast<const uint16_t*>(row)[a])) : 0.f;
+    const int va = tgt_ok ? (a >> 3) : -1;
+
+    uint4 v[kVecPerThread];
+#pragma unroll
+    for (int i = 0; i < kVecPerThread; ++i) {
+      const int idx = tid + i * kCtaThreads;
+      v[i] = idx < nvec ? rv[idx] : make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);
+    }
+
+    float e[kVecPerThread * 8];
+    float mws = 0.f;
+    const int buf = int(k & 1);
+    if (MODE != MODE_BWD) {
+      uint32_t mm = 0xff80ff80u;
+#pragma unroll
+      for (int i = 0; i < kVecPerThread; ++i) {
+        mm = bmax2(mm, v[i].x);
+        mm = bmax2(mm, v[i].y);
+        mm = bmax2(mm, v[i].z);
+        mm = bmax2(mm, v[i].w);
+      }
+      const float mw = warp_max(fmaxf(bf_lo(mm), bf_hi(mm)));
+      mws = (mw == -INFINITY) ? 0.f : mw;
+      const float nmL = -mws * L2E;
+      float s = 0.f, et = 0.f;
+#pragma unroll
+      for (int i = 0; i < kVecPerThread; ++i) {
+        const uint32_t w4[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float t0 = fmaf(bf_lo(w4[q]), L2E, nmL);
+          const float t1 = fmaf(bf_hi(w4[q]), L2E, nmL);
+          const float e0 = ex2(t0), e1 = ex2(t1);
+          e[i * 8 + 2 * q] = e0;
+          e[i * 8 + 2 * q + 1] = e1;
+          s += e0 + e1;
+          et = fmaf(e0, fmaxf(t0, -256.f), et);
+          et = fmaf(e1, fmaxf(t1, -256.f), et);
+        }
+      }
+      if (va >= 0 && (va & (kCtaThreads - 1)) == tid) {
+        // owner of the target column: recompute its partial sums without the target so
+        // that 1 - p_a = S_rest / S keeps full relative precision near saturation
+        s = 0.f;
+        et = 0.f;
+        const uint16_t* rh = reinterpret_cast<const uint16_t*>(row);
+        for (int i = 0; i < kVecPerThread; ++i) {
+          const int idx = tid + i * kCtaThreads;
+          if (idx >= nvec) break;
+          for (int j = 0; j < 8; ++j) {
+            if (idx * 8 + j == a) continue;
+            const float t = fmaf(bf_lo(uint32_t(rh[idx * 8 + j])), L2E, nmL);
+            const float ee = ex2(t);
+            s += ee;
+            et = fmaf(ee, fmaxf(t, -256.f), et);
+          }
+        }
+      }
+      s = warp_sum(s);
+      et = warp_sum(et);
+      if (lane == 0) red[buf * 32 + warp] = make_float4(mw, s, et, 0.f);
+    }
+    __syncthreads();  // stage `st` fully consumed; warp partials visible
+    if (tid == 0 && k + nstages < nrow) {
+      fence_proxy_async();
+      issue_row<MODE>(p, first + (k + nstages) * stride, rowbuf + size_t(st) * stage_bytes,
+                      &meta[st], &full[st], row_bytes, pol);
+    }
+
+    float g, kscale = 0.f, ga = 0.f, lse_row;
+    if (MODE != MODE_BWD) {
+      const float4 q = red[buf * 32 + lane];
+      const float M = warp_max(q.x);
+      const float sc = ex2((q.x - M) * L2E);
+      const float Srest = warp_sum(q.y * sc);
+      const float mq = (q.x == -INFINITY) ? 0.f : q.x;
+      const float Cw = sc * (q.z + (mq - M) * L2E * q.y);
+      const float Csum = warp_sum(Cw);
+      const float ta = (xa - M) * L2E;
+      const float ea = tgt_ok ? ex2(ta) : 0.f;
+      const float Stot = Srest + ea;
+      const float lnS = __logf(Stot);
+      lse_row = M + lnS;
+      const float logp = (xa - M) - lnS;
+      const float Ctot = Csum + (tgt_ok ? ea * fmaxf(ta, -256.f) : 0.f);
+      const float H = lnS - Ctot / (L2E * Stot);
+      g = finish_row<MODE>(p, pc, r, a, lse_row, logp, H, lpb, lpp, advv, ver, key, tid == 0,
+                           want_stats ? sacc : nullptr);
+      const float invS = 1.f / Stot;
+      const float cown = ex2((mws - M) * L2E);
+      kscale = -g * cown * invS;
+      ga = g * Srest * invS;  // dx at the target column: g (1 - p_a)
+    } else {
+      g = tgt_ok ? g_in : 0.f;
+      lse_row = lse_in;
+    }
+
+    if (p.dx != nullptr && MODE != MODE_FWD) {
+      __nv_bfloat16* drow = static_cast<__nv_bfloat16*>(p.dx) + r * p.ld;
+      const float nlL = -lse_row * L2E;
+#pragma unroll
+      for (int i = 0; i < kVecPerThread; ++i) {
+        const int idx = tid + i * kCtaThreads;
+        if (idx < nvec) {
+          uint4 o = make_uint4(0u, 0u, 0u, 0u);
+          if (g != 0.f) {
+            float d[8];
+            if (MODE == MODE_BWD) {
+              const uint32_t w4[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                d[2 * q] = -g * ex2(fmaf(bf_lo(w4[q]), L2E, nlL));
+                d[2 * q + 1] = -g * ex2(fmaf(bf_hi(w4[q]), L2E, nlL));
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) d[j] = kscale * e[i * 8 + j];
+            }
+            o.x = pack_bf16x2(d[0], d[1]);
+            o.y = pack_bf16x2(d[2], d[3]);
+            o.z = pack_bf16x2(d[4], d[5]);
+            o.w = pack_bf16x2(d[6], d[7]);
+            if (idx == va) {
+              // target column: g (1 - p_a)
+              float dv;
+              if (MODE == MODE_BWD) dv = g * (1.f - ex2(fmaf(xa, L2E, nlL)));
+              else dv = ga;
+              const uint32_t hb = uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(dv)));
+              const int qd = (a & 7) >> 1, hf = a & 1;
+              uint32_t* ow = &o.x;
+#pragma unroll
+              for (int z = 0; z < 4; ++z)
+                if (z == qd) ow[z] = hf ? ((ow[z] & 0x0000ffffu) | (hb << 16)) : ((ow[z] & 0xffff0000u) | hb);
+            }
+          }
+          stg_stream(reinterpret_cast<uint4*>(drow) + idx, o);
+        }
+      }
+    }
+  }
+
+  if (want_stats) {
+    __syncthreads();
+    finish_loss_stats(sacc, p.stats, p.partials, p.ctrl, Nden);
+  }
+}
+
+// =====================================================================================
+// small V: one warp per row, register-resident
+// =====================================================================================
+template <typename T, int NV, int MODE>
+__global__ void __launch_bounds__(256) lp_warp_kernel(Lp p) {
+  constexpr int VW = 16 / int(sizeof(T));  // elements per 16-byte vector
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int V = p.V, nvec = V / VW;
+  const float L2E = kLog2e;
+  const bool want_stats = p.stats != nullptr && MODE != MODE_BWD;
+  PpoConst pc;
+  const double Nden = resolve_pc<MODE>(p, pc);
+  double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const int64_t gw = int64_t(blockIdx.x) * 8 + warp, nw = int64_t(gridDim.x) * 8;
+  for (int64_t r = gw; r < p.rows; r += nw) {
+    const T* xr = static_cast<const T*>(p.x) + r * p.ld;
+    const int a = p.target[r];
+    const bool tgt_ok = unsigned(a) < unsigned(V);
+    float x[NV * VW];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int idx = lane + 32 * i;
+      if (idx < nvec) {
+        const uint4 u = ldg_stream(reinterpret_cast<const uint4*>(xr) + idx);
+        const T* tv = reinterpret_cast<const T*>(&u);
+#pragma unroll
+        for (int j = 0; j < VW; ++j) x[i * VW + j] = to_f<T>(tv[j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < VW; ++j) x[i * VW + j] = -INFINITY;
+      }
+    }
+    const float xa = tgt_ok ? to_f<T>(xr[a]) : 0.f;
+    float g = 0.f, lse_row = 0.f, M = 0.f, Stot = 1.f, Srest = 0.f;
+    if (MODE != MODE_BWD) {
+      float mt = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < NV * VW; ++j) mt = fmaxf(mt, x[j]);
+      M = warp_max(mt);
+      const float Ms = (M == -INFINITY) ? 0.f : M;
+      const float nmL = -Ms * L2E;
+      float s = 0.f, et = 0.f;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+#pragma unroll
+        for (int j = 0; j < VW; ++j) {
+          const int col = (lane + 32 * i) * VW + j;
+          const float t = fmaf(x[i * VW + j], L2E, nmL);
+          const float ee = ex2(t);
+          x[i * VW + j] = ee;  // keep e_j in place of x_j
+          if (col != a) {
+            s += ee;
+            et = fmaf(ee, fmaxf(t, -256.f), et);
+          }
+        }
+      }
+      Srest = warp_sum(s);
+      const float Cs = warp_sum(et);
+      const float ta = (xa - Ms) * L2E;
+      const float ea = tgt_ok ? ex2(ta) : 0.f;
+      Stot = Srest + ea;
+      const float lnS = __logf(Stot);
+      lse_row = M + lnS;
+      const float logp = (xa - M) - lnS;
+      const float H = lnS - (Cs + (tgt_ok ? ea * fmaxf(ta, -256.f) : 0.f)) / (L2E * Stot);
+      float lpb = 0.f, lpp = 0.f, advv = 0.f;
+      int ver = 0;
+      uint64_t key = 1;
+      if (MODE == MODE_FUSED) {
+        const int64_t sidx = r / p.A;
+        lpb = p.lpb[r];
+        if (p.lpp) lpp = p.lpp[r];
+        advv = p.adv[sidx];
+        ver = p.ver[sidx];
+        key = p.key[sidx];
+      }
+      g = finish_row<MODE>(p, pc, r, a, lse_row, logp, H, lpb, lpp, advv, ver, key, lane == 0,
+                           want_stats ? acc : nullptr);
+    } else {
+      g = tgt_ok ? p.g_in[r] : 0.f;
+      lse_row = p.lse_in[r];
+    }
+    if (p.dx != nullptr && MODE != MODE_FWD) {
+      T* dr = static_cast<T*>(p.dx) + r * p.ld;
+      const float invS = 1.f / Stot;
+      const float nlL = -lse_row * L2E;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int idx = lane + 32 * i;
+        if (idx < nvec) {
+          uint4 u;
+          T* tv = reinterpret_cast<T*>(&u);
+#pragma unroll
+          for (int j = 0; j < VW; ++j) {
+            const int col = idx * VW + j;
+            float d;
+            if (g == 0.f) {
+              d = 0.f;
+            } else if (MODE == MODE_BWD) {
+              const float pj = ex2(fmaf(x[i * VW + j], L2E, nlL));
+              d = (col == a) ? g * (1.f - pj) : -g * pj;
+            } else {
+              d = (col == a) ? g * Srest * invS : -g * x[i * VW + j] * invS;
+            }
+            tv[j] = from_f<T>(d);
+          }
+          stg_stream(reinterpret_cast<uint4*>(dr) + idx, u);
+        }
+      }
+    }
+  }
+  if (want_stats) {
+    __shared__ double red[8][9];
+    __shared__ double cta[9];
+    if (lane == 0)
+      for (int k = 0; k < 9; ++k) red[warp][k] = acc[k];
+    __syncthreads();
+    if (threadIdx.x < 9) {
+      double s = 0;
+      for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
+      cta[threadIdx.x] = s;
+    }
+    __syncthreads();
+    finish_loss_stats(cta, p.stats, p.partials, p.ctrl, Nden);
+  }
+}
+
+// =====================================================================================
+// generic: any V / ld / alignment / dtype; one CTA per row, three passes over the row
+// =====================================================================================
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) lp_generic_kernel(Lp p) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int V = p.V;
+  const float L2E = kLog2e;
+  const bool want_stats = p.stats != nullptr && MODE != MODE_BWD;
+  PpoConst pc;
+  const double Nden = resolve_pc<MODE>(p, pc);
+  __shared__ float redf[2][8];
+  __shared__ double sacc[16];
+  if (tid < 16) sacc[tid] = 0.0;
+  __syncthreads();
+  for (int64_t r = blockIdx.x; r < p.rows; r += gridDim.x) {
+    const T* xr = static_cast<const T*>(p.x) + r * p.ld;
+    const int a = p.target[r];
+    const bool tgt_ok = unsigned(a) < unsigned(V);
+    const float xa = tgt_ok ? to_f<T>(xr[a]) : 0.f;
+    float g, lse_row, Stot = 1.f, Srest = 0.f, Ms = 0.f;
+    if (MODE != MODE_BWD) {
+      float mt = -INFINITY;
+      for (int j = tid; j < V; j += 256) mt = fmaxf(mt, to_f<T>(xr[j]));
+      mt = warp_max(mt);
+      if (lane == 0) redf[0][warp] = mt;
+      __syncthreads();
+      float M = redf[0][0];
+      for (int w = 1; w < 8; ++w) M = fmaxf(M, redf[0][w]);
+      Ms = (M == -INFINITY) ? 0.f : M;
+      const float nmL = -Ms * L2E;
+      float s = 0.f, et = 0.f;
+      for (int j = tid; j < V; j += 256) {
+        if (j == a) continue;
+        const float t = fmaf(to_f<T>(xr[j]), L2E, nmL);
+        const float ee = ex2(t);
+        s += ee;
+        et = fmaf(ee, fmaxf(t, -256.f), et);
+      }
+      s = warp_sum(s);
+      et = warp_sum(et);
+      __syncthreads();
+      if (lane == 0) {
+        redf[0][warp] = s;
+        redf[1][warp] = et;
+      }
+      __syncthreads();
+      Srest = 0.f;
+      float Cs = 0.f;
+      for (int w = 0; w < 8; ++w) {
+        Srest += redf[0][w];
+        Cs += redf[1][w];
+      }
+      const float ta = (xa - Ms) * L2E;
+      const float ea = tgt_ok ? ex2(ta) : 0.f;
+      Stot = Srest + ea;
+      const float lnS = __logf(Stot);
+      lse_row = M + lnS;
+      const float logp = (xa - M) - lnS;
+      const float H = lnS - (Cs + (tgt_ok ? ea * fmaxf(ta, -256.f) : 0.f)) / (L2E * Stot);
+      float lpb = 0.f, lpp = 0.f, advv = 0.f;
+      int ver = 0;
+      uint64_t key = 1;
+      if (MODE == MODE_FUSED) {
+        const int64_t sidx = r / p.A;
+        lpb = p.lpb[r];
+        if (p.lpp) lpp = p.lpp[r];
+        advv = p.adv[sidx];
+        ver = p.ver[sidx];
+        key = p.key[sidx];
+      }
+      g = finish_row<MODE>(p, pc, r, a, lse_row, logp, H, lpb, lpp, advv, ver, key, tid == 0,
+                           want_stats ? sacc : nullptr);
+    } else {
+      g = tgt_ok ? p.g_in[r] : 0.f;
+      lse_row = p.lse_in[r];
+    }
+    if (p.dx != nullptr && MODE != MODE_FWD) {
+      T* dr = static_cast<T*>(p.dx) + r * p.ld;
+      const float invS = 1.f / Stot;
+      const float nmL = -Ms * L2E, nlL = -lse_row * L2E;
+      for (int j = tid; j < V; j += 256) {
+        const float xj = to_f<T>(xr[j]);
+        float d;
+        if (g == 0.f) d = 0.f;
+        else if (MODE == MODE_BWD) {
+          const float pj = ex2(fmaf(xj, L2E, nlL));
+          d = (j == a) ? g * (1.f - pj) : -g * pj;
+        } else {
+          d = (j == a) ? g * Srest * invS : -g * ex2(fmaf(xj, L2E, nmL)) * invS;
+        }
+        dr[j] = from_f<T>(d);
+      }
+    }
+    __syncthreads();  // redf reuse across rows
+  }
+  if (want_stats) {
+    __syncthreads();
+    finish_loss_stats(sacc, p.stats, p.partials, p.ctrl, Nden);
+  }
+}
+
+Lp make_lp(const LpArgs& a) {
+  Lp p{};
+  p.x = a.x.ptr;
+  p.rows = a.x.rows;
+  p.V = a.x.vocab;
+  p.ld = a.x.ld;
+  p.target = a.target;
+  p.logp = a.logp;
+  p.lse_out = a.grad_logp ? nullptr : a.lse;
+  p.lse_in = a.grad_logp ? a.lse : nullptr;
+  p.g_in = a.grad_logp;
+  p.dx = a.dlogits;
+  p.stats = a.stats;
+  p.partials = a.ws.partials;
+  p.ctrl = a.ws.ctrl + CTRL_LOGPROB;
+  if (a.fused) {
+    p.lpb = a.f.logp_behav;
+    p.lpp = a.f.logp_prox;
+    p.adv = a.f.adv;
+    p.ver = a.f.version;
+    p.key = a.f.slot_key;
+    p.A = a.f.a_tok;
+    p.pc.has_prox = a.f.logp_prox != nullptr;
+    p.pc.cur_version = a.f.cur_version;
+    p.pc.eta = a.f.max_staleness;
+    p.pc.lo = 1.f - a.f.eps_low;
+    p.pc.hi = 1.f + a.f.eps_high;
+    p.pc.is_cap = a.f.is_cap;
+    p.out_g = a.f.out_grad_logp;
+    p.out_L = a.f.out_loss_tok;
+    p.N = a.f.tok_denominator;
+    p.adv_stats = a.f.adv_stats;
+  }
+  return p;
+}
+
+template <int MODE>
+cudaError_t launch_mode(const LpArgs& a, Lp p, cudaStream_t s) {
+  const LpPath path = select_lp_path(a);
+  const int sms = device_info().sm_count;
+  const int64_t R = a.x.rows;
+  if (R <= 0) return cudaSuccess;
+  if (path == LP_PATH_TMA) {
+    const uint32_t row_bytes = uint32_t(a.x.vocab) * 2u;
+    const uint32_t stage_bytes = (row_bytes + 127u) & ~127u;
+    const size_t fixed = kMaxStages * sizeof(StageMeta) + kMaxStages * 8 + 64 * sizeof(float4) +
+                         16 * sizeof(double);
+    int nst = int((size_t(device_info().smem_optin) - fixed - 1024) / stage_bytes);
+    if (nst > kMaxStages) nst = kMaxStages;
+    if (nst < 2) return cudaErrorInvalidConfiguration;
+    const size_t smem = size_t(nst) * stage_bytes + fixed;
+    static bool attr_set[3] = {false, false, false};
+    if (!attr_set[MODE]) {
+      cudaError_t e = cudaFuncSetAttribute(lp_tma_kernel<MODE>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(device_info().smem_optin));
+      if (e != cudaSuccess) return e;
+      attr_set[MODE] = true;
+    }
+    int grid = int(R < sms ? R : sms);
+    lp_tma_kernel<MODE><<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);
+    return cudaGetLastError();
+  }
+  if (path == LP_PATH_WARP) {
+    const int VW = a.x.dtype == RLVLA_BF16 ? 8 : 4;
+    const int nv = (a.x.vocab / VW + 31) / 32;  // vectors per lane
+    int64_t blocks = (R + 7) / 8;
+    const int64_t cap = int64_t(sms) * 8;
+    if (blocks > cap) blocks = cap;
+    const int g = int(blocks);
+    if (a.x.dtype == RLVLA_BF16) {
+      if (nv <= 1) lp_warp_kernel<__nv_bfloat16, 1, MODE><<<g, 256, 0, s>>>(p);
+      else if (nv <= 4) lp_warp_kernel<__nv_bfloat16, 4, MODE><<<g, 256, 0, s>>>(p);
+      else lp_warp_kernel<__nv_bfloat16, 8, MODE><<<g, 256, 0, s>>>(p);
+    } else {
+      if (nv <= 2) lp_warp_kernel<float, 2, MODE><<<g, 256, 0, s>>>(p);
+      else if (nv <= 4) lp_warp_kernel<float, 4, MODE><<<g, 256, 0, s>>>(p);
+      else lp_warp_kernel<float, 8, MODE><<<g, 256, 0, s>>>(p);
+    }
+    return cudaGetLastError();
+  }
+  int64_t blocks = R;
+  const int64_t cap = int64_t(sms) * 8;
+  if (blocks > cap) blocks = cap;
+  if (a.x.dtype == RLVLA_BF16) lp_generic_kernel<__nv_bfloat16, MODE><<<int(blocks), 256, 0, s>>>(p);
+  else lp_generic_kernel<float, MODE><<<int(blocks), 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+LpPath select_lp_path(const LpArgs& a) {
+  const int V = a.x.vocab;
+  const int VW = a.x.dtype == RLVLA_BF16 ? 8 : 4;
+  const uintptr_t xp = reinterpret_cast<uintptr_t>(a.x.ptr);
+  const uintptr_t dp = reinterpret_cast<uintptr_t>(a.dlogits);
+  const bool aligned = (xp % 16 == 0) && (dp % 16 == 0) && (V % VW == 0) && (a.x.ld % VW == 0);
+  if (!aligned) return LP_PATH_GENERIC;
+  if (V <= 32 * 8 * VW && V / VW <= 256) return LP_PATH_WARP;
+  if (a.x.dtype == RLVLA_BF16 && V <= kCtaThreads * kVecPerThread * 8) return LP_PATH_TMA;
+  return LP_PATH_GENERIC;
+}
+
+cudaError_t launch_logprob(const LpArgs& a, cudaStream_t s) {
+  const Lp p = make_lp(a);
+  if (a.fused) return launch_mode<MODE_FUSED>(a, p, s);
+  if (a.grad_logp) return launch_mode<MODE_BWD>(a, p, s);
+  return launch_mode<MODE_FWD>(a, p, s);
+}
+
+}  // namespace rlvla

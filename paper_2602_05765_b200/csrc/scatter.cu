@@ -1,0 +1,154 @@
+// scatter.cu — S1: out-of-order step records -> trajectory buffer (K1a claim, K1b write).
+//
+// Paper: trajectories carry their policy version (§3.1); requests from subsets of
+// envs arrive early / out of order (§3.2); samples accumulate in the trajectory
+// buffer (§3.3). Reading R6: sequential-replay semantics with
+// key = (version << 40) | seq, newest key wins, every extra arrival is a duplicate.
+//
+// GPU formulation (thread-order independent, hence bit-exact vs the replay):
+//   claim: one thread per record; u64 atomicMax(slot_key, key) returns the previous key.
+//          Exactly one valid record per slot per call observes the pre-call key, so
+//          written = #(old == 0) and dup = #(old != 0) match the replay counts.
+//   write: after all claims, a record whose key equals the slot's final key is the unique
+//          winner and copies its payload (one warp per record, coalesced over a_tok).
+// M <= 1024 (an Eq. (1) arrival chunk, B_max = 64 in the paper's setting) runs as one
+// CTA (claim, __syncthreads, write) — one launch; larger M uses two grid launches.
+#include "internal.cuh"
+
+namespace rlvla {
+namespace {
+
+constexpr int kVersionShift = 40;
+
+struct Claim {
+  int valid;
+  uint64_t key;
+  int64_t slot;
+};
+
+__device__ __forceinline__ Claim claim_one(const ScatterArgs& a, int i, long long cnt[4]) {
+  Claim c{0, 0, 0};
+  const int e = a.rec.env_id[i];
+  const int t = a.rec.step[i];
+  const int v = a.rec.version[i];
+  if (e < 0 || e >= a.buf.n_env || t < 0 || t >= a.buf.t_steps) {
+    cnt[RLVLA_CNT_OOB] += 1;
+    return c;
+  }
+  if (v < 0 || v > a.cur_version) {
+    cnt[RLVLA_CNT_BAD_VERSION] += 1;
+    return c;
+  }
+  c.slot = int64_t(e) * a.buf.t_steps + t;
+  c.key = (uint64_t(uint32_t(v)) << kVersionShift) | (a.seq_base + uint64_t(i));
+  unsigned long long old = atomicMax(reinterpret_cast<unsigned long long*>(a.buf.slot_key + c.slot),
+                                     static_cast<unsigned long long>(c.key));
+  if (old != 0ull) cnt[RLVLA_CNT_DUP] += 1;
+  else cnt[RLVLA_CNT_WRITTEN] += 1;
+  c.valid = 1;
+  return c;
+}
+
+// warp-cooperative payload copy of record i into slot (winner only)
+__device__ __forceinline__ void write_payload(const ScatterArgs& a, int i, int64_t slot, int lane) {
+  const int A = a.buf.a_tok;
+  if (lane == 0) {
+    a.buf.reward[slot] = a.rec.reward[i];
+    a.buf.done[slot] = a.rec.done[i];
+    a.buf.value[slot] = a.rec.value[i];
+    a.buf.version[slot] = a.rec.version[i];
+  }
+  const int32_t* st = a.rec.tokens + int64_t(i) * A;
+  const float* sl = a.rec.logp_behav + int64_t(i) * A;
+  int32_t* dt = a.buf.tokens + slot * A;
+  float* dl = a.buf.logp_behav + slot * A;
+  for (int j = lane; j < A; j += 32) {
+    dt[j] = st[j];
+    dl[j] = sl[j];
+  }
+}
+
+__device__ __forceinline__ void block_add_counters(long long cnt[4], int64_t* counters) {
+  __shared__ long long red[32][4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) cnt[k] = warp_sum_ll(cnt[k]);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) red[warp][k] = cnt[k];
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    long long s = 0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) s += red[w][threadIdx.x];
+    if (s) atomicAdd(reinterpret_cast<unsigned long long*>(counters + threadIdx.x),
+                     static_cast<unsigned long long>(s));
+  }
+}
+
+// M <= 1024: claim + write in one CTA
+__global__ void __launch_bounds__(1024) scatter_fused_kernel(ScatterArgs a) {
+  const int i = threadIdx.x;
+  const int M = a.rec.n_rec;
+  long long cnt[4] = {0, 0, 0, 0};
+  if (i < M) (void)claim_one(a, i, cnt);
+  __syncthreads();  // all claims (device-scope atomics) issued by this CTA are done
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int r = warp; r < M; r += nw) {
+    const int e = a.rec.env_id[r], t = a.rec.step[r], v = a.rec.version[r];
+    if (e < 0 || e >= a.buf.n_env || t < 0 || t >= a.buf.t_steps || v < 0 || v > a.cur_version)
+      continue;
+    const int64_t slot = int64_t(e) * a.buf.t_steps + t;
+    const uint64_t key = (uint64_t(uint32_t(v)) << kVersionShift) | (a.seq_base + uint64_t(r));
+    if (__ldcg(reinterpret_cast<const unsigned long long*>(a.buf.slot_key + slot)) == key)
+      write_payload(a, r, slot, lane);
+  }
+  block_add_counters(cnt, a.counters);
+}
+
+__global__ void __launch_bounds__(256) scatter_claim_kernel(ScatterArgs a) {
+  long long cnt[4] = {0, 0, 0, 0};
+  const int M = a.rec.n_rec;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < M; i += gridDim.x * blockDim.x)
+    (void)claim_one(a, i, cnt);
+  block_add_counters(cnt, a.counters);
+}
+
+__global__ void __launch_bounds__(256) scatter_write_kernel(ScatterArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int r = gw; r < a.rec.n_rec; r += nw) {
+    const int e = a.rec.env_id[r], t = a.rec.step[r], v = a.rec.version[r];
+    if (e < 0 || e >= a.buf.n_env || t < 0 || t >= a.buf.t_steps || v < 0 || v > a.cur_version)
+      continue;
+    const int64_t slot = int64_t(e) * a.buf.t_steps + t;
+    const uint64_t key = (uint64_t(uint32_t(v)) << kVersionShift) | (a.seq_base + uint64_t(r));
+    if (__ldcg(reinterpret_cast<const unsigned long long*>(a.buf.slot_key + slot)) == key)
+      write_payload(a, r, slot, lane);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s) {
+  const int M = a.rec.n_rec;
+  if (M <= 0) return cudaSuccess;
+  if (M <= 1024) {
+    int threads = ((M + 31) / 32) * 32;
+    if (threads < 64) threads = 64;
+    scatter_fused_kernel<<<1, threads, 0, s>>>(a);
+    return cudaGetLastError();
+  }
+  const int sms = device_info().sm_count;
+  int blocks = (M + 255) / 256;
+  if (blocks > 8 * sms) blocks = 8 * sms;
+  scatter_claim_kernel<<<blocks, 256, 0, s>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  int wblocks = (M + 7) / 8;
+  if (wblocks > 16 * sms) wblocks = 16 * sms;
+  scatter_write_kernel<<<wblocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace rlvla

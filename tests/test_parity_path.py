@@ -1,0 +1,137 @@
+"""GPU parity: the whole rollout-to-loss path (S1 -> S2 -> S3+S4) through the C ABI vs the
+oracle, element by element, on the tiny config (everything) and on a LIBERO-OFT-shaped
+reduction (bf16 V=32000, TMA path; S1/S2 in full, S3/S4 on every row of a few envs)."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import path as O_path
+from tests import harness as H
+
+pytestmark = pytest.mark.gpu
+
+CUR = synth.CUR_VERSION
+
+
+def _run_gpu_path(case, mode, buf, whiten=False, tok_den=0.0):
+    import paper_2602_05765_b200 as P
+    cfg = case.cfg
+    E, T, A = case.n_env, cfg.t_steps, cfg.a_tok
+    dev = "cuda"
+    ws = P.workspace(E, device=dev)
+    stats = torch.zeros(16, dtype=torch.float64, device=dev)
+    adv = torch.zeros(E, T, dtype=torch.float32, device=dev)
+    ret = torch.zeros(E, T, dtype=torch.float32, device=dev)
+    lv = torch.from_numpy(case.traj.last_value[case.env_lo:case.env_hi]).to(dev)
+    gid = torch.from_numpy(case.traj.group_id).to(dev)
+    prm = P.adv_params(mode, whiten=whiten, group_id=gid if mode == "grpo" else None,
+                       group_size=cfg.group_size, n_env_global=E, cur_version=CUR,
+                       max_staleness=1)
+    P.rlvla_advantages(buf, lv, prm, adv, ret, stats, ws)
+    R = E * T * A
+    logits = case.logits.to(dev)
+    logp = torch.empty(R, dtype=torch.float32, device=dev)
+    lse = torch.empty(R, dtype=torch.float32, device=dev)
+    g = torch.empty(R, dtype=torch.float32, device=dev)
+    lt = torch.empty(R, dtype=torch.float32, device=dev)
+    dx = torch.empty_like(logits)
+    fa = P.ppo_args(logp_behav=buf.logp_behav.view(-1), adv=adv.view(-1), version=buf.version.view(-1),
+                    slot_key=buf.slot_key.view(-1), a_tok=A, cur_version=CUR, max_staleness=1,
+                    tok_denominator=tok_den, adv_stats=stats, out_grad_logp=g, out_loss_tok=lt)
+    st2 = torch.zeros(16, dtype=torch.float64, device=dev)
+    P.rlvla_logprob_fwd_bwd(logits, buf.tokens.view(-1), logp=logp, lse=lse, fused=fa,
+                            dlogits=dx, stats=st2, ws=ws)
+    torch.cuda.synchronize()
+    stats_all = stats.cpu().numpy().copy()
+    stats_all[6:] = st2.cpu().numpy()[6:]
+    return dict(adv=adv.cpu().numpy(), ret=ret.cpu().numpy(), logp=logp.cpu().numpy(),
+                lse=lse.cpu().numpy(), g=g.cpu().numpy(), lt=lt.cpu().numpy(), dx=dx,
+                stats=stats_all)
+
+
+def _compare_path(case, mode, whiten=False, rows=None):
+    cfg = case.cfg
+    # S1: bit-exact buffer and counters
+    gbuf, gcnt = H.gpu_scatter(case)
+    obuf, ocnt = H.oracle_scatter(case)
+    gb = H.buf_to_np(gbuf)
+    for k in obuf:
+        assert np.array_equal(gb[k].view(np.uint8), obuf[k].view(np.uint8)), f"buffer.{k}"
+    assert gcnt.cpu().numpy().tolist() == ocnt.tolist()
+    out = _run_gpu_path(case, mode, gbuf, whiten=whiten)
+    # S2
+    oadv = H.oracle_advantages(case, obuf, mode, whiten=whiten)
+    floor = max(1e-3, float(np.sqrt(np.mean(oadv["adv"] ** 2))))
+    H.assert_close_rel(out["adv"], oadv["adv"], 1e-5, floor, "adv")
+    H.assert_close_rel(out["ret"], oadv["ret"], 1e-5, floor, "ret")
+    c = oadv["counts"]
+    st = out["stats"]
+    assert st[0] == c["n_valid"] and st[3] == c["n_tok"] and st[4] == c["n_stale"] and st[5] == c["n_bad"]
+    # S3+S4 on `rows` (all by default), compared chunk by chunk
+    tv = O_path.token_view(obuf, oadv["adv"], cfg.a_tok, CUR)
+    rows = np.arange(len(tv["target"])) if rows is None else rows
+    refs = []
+    for s in range(0, len(rows), 2048):
+        rr = rows[s:s + 2048]
+        refs.append(_compare_rows(case, out, tv, rr, float(c["n_tok"])))
+    ref = _merge(refs)
+    return out, ref, oadv
+
+
+def _compare_rows(case, out, tv, rows, n_tok):
+    xr = case.logits[torch.from_numpy(rows).to(case.logits.device)].double().cpu().numpy()
+    ref = O_path.loss_and_grad(xr, tv, n_tok=n_tok, rows=rows)
+    f, p = ref["fwd"], ref["ppo"]
+    H.assert_close_rel(out["logp"][rows], f["logp"], 1e-5, 1.0, "logp")
+    fin = np.isfinite(f["lse"])
+    H.assert_close_rel(out["lse"][rows][fin], f["lse"][fin], 1e-5, 1.0, "lse")
+    # near-ties (|rho/bound - 1| <= 1e-5) may take either branch (reading R11)
+    nt = p["near_tie"]
+    gscale = max(1e-30, float(np.abs(p["grad"]).max()))
+    H.assert_close_rel(out["g"][rows][~nt], p["grad"][~nt], 1e-5, gscale * 1e-3, "grad_logp")
+    H.assert_close_rel(out["lt"][rows], p["loss_tok"], 1e-5, 1e-3, "loss_tok")
+    dx = out["dx"][torch.from_numpy(rows).cuda()]
+    if case.logits.dtype == torch.bfloat16:
+        bits = dx.view(torch.int16).cpu().numpy().astype(np.int32) & 0xFFFF
+        H.assert_bf16_ulp(bits[~nt], ref["dx"][~nt], 1)
+    else:
+        d = dx.cpu().numpy()
+        rowscale = np.abs(ref["dx"]).max(axis=1, keepdims=True)
+        H.assert_close_rel(d[~nt], ref["dx"][~nt], 1e-5, np.maximum(rowscale[~nt] * 1e-6, 1e-30),
+                           "dlogits")
+    return dict(stats=ref["stats"], near_tie=int(nt.sum()))
+
+
+def _merge(refs):
+    st = {k: sum(r["stats"][k] for r in refs) for k in refs[0]["stats"] if k != "denom"}
+    st["denom"] = refs[0]["stats"]["denom"]
+    return dict(stats=st, near_tie=sum(r["near_tie"] for r in refs))
+
+
+def test_tiny_full_path_grpo():
+    case = H.build_case(synth.CONFIGS["tiny"], device="cpu")
+    out, ref, oadv = _compare_path(case, "grpo")
+    st, rs = out["stats"], ref["stats"]
+    assert abs(st[6] - rs["loss"]) <= 1e-5 * max(1.0, abs(rs["loss"]))
+    for slot, key in ((8, "kl_k3_sum"), (9, "entropy_sum"), (10, "ratio_sum"), (14, "logp_sum")):
+        assert abs(st[slot] - rs[key]) <= 1e-5 * max(1.0, abs(rs[key])), key
+    assert st[11] == rs["n_loss_tok"] and st[12] == rs["n_stale_tok"] and st[13] == rs["n_bad_tok"]
+    assert abs(st[7] - rs["n_clipped"]) <= ref["near_tie"]
+    assert st[15] == oadv["counts"]["n_tok"]
+    # the fault injections really happened
+    assert rs["n_stale_tok"] > 0 and rs["n_bad_tok"] == 0
+
+
+def test_tiny_full_path_gae_whitened():
+    case = H.build_case(synth.CONFIGS["tiny"], device="cpu")
+    _compare_path(case, "gae", whiten=True)
+
+
+def test_oft_shape_reduced_tma_path():
+    """LIBERO-Spatial OFT recipe (bf16, V=32000, A=56, T=64) on 2 envs: S1/S2 in full,
+    S3/S4 on every row (7,168 rows x 32000)."""
+    cfg = synth.scaled(synth.CONFIGS["libero_spatial_oft"], n_env=2)
+    case = H.build_case(cfg, device="cuda")
+    out, ref, _ = _compare_path(case, "grpo")
+    assert np.abs(out["logp"] - 0).max() > 0
