@@ -11,6 +11,9 @@ write it out. Two-pass definition, float64:
     logp = x_a - lse
     H   = lse - sum_j p_j x_j          (p_j = exp(x_j - lse); p_j x_j := 0 where p_j = 0)
     dx_j = g * (1[j = a] - p_j)        (backward with upstream g = dL/dlogp)
+           at j = a the factor 1 - p_a is evaluated as sum_{j != a} p_j (the same number;
+           written this way because 1 - p_a cancels to 0 in float64 once p_a > 1 - 1e-16,
+           e.g. a saturated row, DESIGN.md §2 reading R15b)
 Readings: R3 (normalise over the V columns supplied), R4 (target -1 = ignore, other
 out-of-range targets counted), R5 (-inf allowed in non-target columns; NaN/+inf or an
 all -inf row give a non-finite result that is counted).
@@ -60,9 +63,11 @@ def log_softmax_grad(x, target, lse, g):
     R, V = x.shape
     with np.errstate(invalid="ignore", over="ignore"):
         p = np.exp(x - np.asarray(lse, np.float64)[:, None])
-    onehot = np.zeros_like(x)
+    dx = -g[:, None] * p
     ok = (tgt >= 0) & (tgt < V)
-    onehot[np.nonzero(ok)[0], tgt[ok]] = 1.0
-    dx = g[:, None] * (onehot - p)
+    for r in np.nonzero(ok)[0]:
+        a = tgt[r]
+        rest = p[r, :a].sum() + p[r, a + 1:].sum()       # = 1 - p_a
+        dx[r, a] = g[r] * rest
     dx[g == 0] = 0.0
     return dx

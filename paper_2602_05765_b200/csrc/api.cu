@@ -3,6 +3,7 @@
 // allgather) and C3 (loss statistics allreduce), all enqueued on the caller's stream.
 #include <nccl.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -58,7 +59,13 @@ size_t ws_bytes_for(int32_t n_env_global) {
   return kCtrlBytes + kPartialBytes + r;
 }
 
-rlvla_status cuda_status(cudaError_t e) { return e == cudaSuccess ? RLVLA_OK : RLVLA_ERR_CUDA; }
+// RLVLA_DEBUG=1 prints the CUDA error behind an RLVLA_ERR_CUDA to stderr
+rlvla_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return RLVLA_OK;
+  const char* d = std::getenv("RLVLA_DEBUG");
+  if (d && d[0] == '1') std::fprintf(stderr, "[rlvla] CUDA error %d: %s\n", int(e), cudaGetErrorString(e));
+  return RLVLA_ERR_CUDA;
+}
 
 bool device_ready() { return device_info().sm_count > 0; }
 

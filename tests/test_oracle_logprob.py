@@ -98,3 +98,17 @@ def test_grad_sums_to_zero_and_finite_differences():
                 fd = g[r] * (L.log_softmax_gather(xp, t)["logp"][r] -
                              L.log_softmax_gather(xm, t)["logp"][r]) / (2 * h)
                 assert abs(fd - dx[r, j]) <= 1e-6 * max(1.0, abs(dx[r, j]))
+
+
+def test_saturated_target_gradient_closed_form():
+    """Target +30, V-1 others -30: 1 - p_a = (V-1)e^-60 / (1 + (V-1)e^-60) (closed form);
+    the oracle must not cancel it to 0 (cf. S:398 saturation example)."""
+    for V in (4, 256, 32000):
+        x = np.full((1, V), -30.0)
+        x[0, 2] = 30.0
+        f = L.log_softmax_gather(x, [2])
+        dx = L.log_softmax_grad(x, [2], f["lse"], [-2.0])
+        q = (V - 1) * np.exp(-60.0)
+        assert abs(dx[0, 2] - (-2.0) * q / (1 + q)) <= 1e-12 * abs(dx[0, 2])
+        assert abs(dx[0, 0] - 2.0 * np.exp(-60.0) / (1 + q)) <= 1e-12 * abs(dx[0, 0])
+        assert abs(dx.sum()) <= 1e-12 * abs(dx[0, 2])
