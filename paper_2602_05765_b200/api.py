@@ -136,9 +136,11 @@ def rlvla_scatter_steps(buf: TrajectoryBuffer, rec: StepBatch, cur_version: int,
 def adv_params(mode, *, gamma=0.99, lam=0.95, whiten=False, whiten_eps=1e-8, group_id=None,
                group_size=0, std_unbiased=True, grpo_eps=1e-6, env_offset=0, n_env_global=0,
                cur_version=0, max_staleness=1) -> A.c_adv_params:
-    return A.c_adv_params(A.ADV_GAE if mode == "gae" else A.ADV_GRPO, gamma, lam, int(whiten),
-                          whiten_eps, _ptr(group_id), group_size, int(std_unbiased), grpo_eps,
-                          env_offset, n_env_global, cur_version, max_staleness)
+    p = A.c_adv_params(A.ADV_GAE if mode == "gae" else A.ADV_GRPO, gamma, lam, int(whiten),
+                       whiten_eps, _ptr(group_id), group_size, int(std_unbiased), grpo_eps,
+                       env_offset, n_env_global, cur_version, max_staleness)
+    p._keep = (group_id,)      # the struct holds raw pointers: keep the tensors alive
+    return p
 
 
 def rlvla_advantages(buf: TrajectoryBuffer, last_value, params: A.c_adv_params, adv, ret,
@@ -161,10 +163,14 @@ def logits_desc(x: torch.Tensor, vocab: int | None = None) -> A.c_logits:
 def ppo_args(*, logp_behav, adv, version, slot_key, a_tok, cur_version, max_staleness=1,
              eps_low=0.2, eps_high=0.2, is_cap=0.0, logp_prox=None, tok_denominator=0.0,
              adv_stats=None, out_grad_logp=None, out_loss_tok=None) -> A.c_ppo_args:
-    return A.c_ppo_args(_ptr(logp_behav), _ptr(logp_prox), _ptr(adv), _ptr(version),
-                        _ptr(slot_key), a_tok, cur_version, max_staleness, eps_low, eps_high,
-                        is_cap, tok_denominator, _ptr(adv_stats), _ptr(out_grad_logp),
-                        _ptr(out_loss_tok))
+    a = A.c_ppo_args(_ptr(logp_behav), _ptr(logp_prox), _ptr(adv), _ptr(version),
+                     _ptr(slot_key), a_tok, cur_version, max_staleness, eps_low, eps_high,
+                     is_cap, tok_denominator, _ptr(adv_stats), _ptr(out_grad_logp),
+                     _ptr(out_loss_tok))
+    # the struct holds raw pointers: keep the tensors alive as long as the struct
+    a._keep = (logp_behav, logp_prox, adv, version, slot_key, adv_stats, out_grad_logp,
+               out_loss_tok)
+    return a
 
 
 def rlvla_logprob_fwd_bwd(x: torch.Tensor, target, logp=None, lse=None, grad_logp=None,

@@ -62,6 +62,7 @@ size_t ws_bytes_for(int32_t n_env_global) {
 // RLVLA_DEBUG=1 prints the CUDA error behind an RLVLA_ERR_CUDA to stderr
 rlvla_status cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return RLVLA_OK;
+  (void)cudaGetLastError();  // do not leave a (non-sticky) error for the next caller
   const char* d = std::getenv("RLVLA_DEBUG");
   if (d && d[0] == '1') std::fprintf(stderr, "[rlvla] CUDA error %d: %s\n", int(e), cudaGetErrorString(e));
   return RLVLA_ERR_CUDA;

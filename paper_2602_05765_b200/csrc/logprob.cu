@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
             if (idx == va) {
               // target column: g (1 - p_a)
               float dv;
-              if (MODE == MODE_BWD) dv = g * (1.f - ex2(fmaf(xa, L2E, nlL)));
+              if (MODE == MODE_BWD) dv = -g * expm1f(xa - lse_row);
               else dv = ga;
               const uint32_t hb = uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(dv)));
               const int qd = (a & 7) >> 1, hf = a & 1;
@@ -468,8 +468,8 @@ __global__ void __launch_bounds__(256) lp_warp_kernel(Lp p) {
             if (g == 0.f) {
               d = 0.f;
             } else if (MODE == MODE_BWD) {
-              const float pj = ex2(fmaf(x[i * VW + j], L2E, nlL));
-              d = (col == a) ? g * (1.f - pj) : -g * pj;
+              d = (col == a) ? -g * expm1f(x[i * VW + j] - lse_row)
+                             : -g * ex2(fmaf(x[i * VW + j], L2E, nlL));
             } else {
               d = (col == a) ? g * Srest * invS : -g * x[i * VW + j] * invS;
             }
@@ -582,8 +582,7 @@ __global__ void __launch_bounds__(256) lp_generic_kernel(Lp p) {
         float d;
         if (g == 0.f) d = 0.f;
         else if (MODE == MODE_BWD) {
-          const float pj = ex2(fmaf(xj, L2E, nlL));
-          d = (j == a) ? g * (1.f - pj) : -g * pj;
+          d = (j == a) ? -g * expm1f(xj - lse_row) : -g * ex2(fmaf(xj, L2E, nlL));
         } else {
           d = (j == a) ? g * Srest * invS : -g * ex2(fmaf(xj, L2E, nmL)) * invS;
         }
@@ -645,17 +644,21 @@ cudaError_t launch_mode(const LpArgs& a, Lp p, cudaStream_t s) {
     const uint32_t stage_bytes = (row_bytes + 127u) & ~127u;
     const size_t fixed = kMaxStages * sizeof(StageMeta) + kMaxStages * 8 + 64 * sizeof(float4) +
                          16 * sizeof(double);
-    int nst = int((size_t(device_info().smem_optin) - fixed - 1024) / stage_bytes);
+    int nst = int((size_t(device_info().smem_optin) - fixed - 2048) / stage_bytes);
     if (nst > kMaxStages) nst = kMaxStages;
     if (nst < 2) return cudaErrorInvalidConfiguration;
     const size_t smem = size_t(nst) * stage_bytes + fixed;
-    static bool attr_set[3] = {false, false, false};
-    if (!attr_set[MODE]) {
-      cudaError_t e = cudaFuncSetAttribute(lp_tma_kernel<MODE>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(device_info().smem_optin));
+    // dynamic smem limit = opt-in max minus the kernel's static smem
+    static int attr_dyn[3] = {0, 0, 0};
+    if (attr_dyn[MODE] < int(smem)) {
+      cudaFuncAttributes fa{};
+      cudaError_t e = cudaFuncGetAttributes(&fa, lp_tma_kernel<MODE>);
       if (e != cudaSuccess) return e;
-      attr_set[MODE] = true;
+      if (smem + fa.sharedSizeBytes > size_t(device_info().smem_optin)) return cudaErrorInvalidConfiguration;
+      e = cudaFuncSetAttribute(lp_tma_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem));
+      if (e != cudaSuccess) return e;
+      attr_dyn[MODE] = int(smem);
     }
     int grid = int(R < sms ? R : sms);
     lp_tma_kernel<MODE><<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);

@@ -14,10 +14,10 @@ pytestmark = pytest.mark.gpu
 CUR = synth.CUR_VERSION
 
 
-def _run_gpu_path(case, mode, buf, whiten=False, tok_den=0.0):
+def _gpu_advantages(case, mode, buf, whiten=False):
     import paper_2602_05765_b200 as P
     cfg = case.cfg
-    E, T, A = case.n_env, cfg.t_steps, cfg.a_tok
+    E, T = case.n_env, cfg.t_steps
     dev = "cuda"
     ws = P.workspace(E, device=dev)
     stats = torch.zeros(16, dtype=torch.float64, device=dev)
@@ -29,6 +29,15 @@ def _run_gpu_path(case, mode, buf, whiten=False, tok_den=0.0):
                        group_size=cfg.group_size, n_env_global=E, cur_version=CUR,
                        max_staleness=1)
     P.rlvla_advantages(buf, lv, prm, adv, ret, stats, ws)
+    torch.cuda.synchronize()
+    return adv, ret, stats, ws
+
+
+def _gpu_loss(case, buf, adv, stats, ws, tok_den=0.0):
+    import paper_2602_05765_b200 as P
+    cfg = case.cfg
+    E, T, A = case.n_env, cfg.t_steps, cfg.a_tok
+    dev = "cuda"
     R = E * T * A
     logits = case.logits.to(dev)
     logp = torch.empty(R, dtype=torch.float32, device=dev)
@@ -45,12 +54,14 @@ def _run_gpu_path(case, mode, buf, whiten=False, tok_den=0.0):
     torch.cuda.synchronize()
     stats_all = stats.cpu().numpy().copy()
     stats_all[6:] = st2.cpu().numpy()[6:]
-    return dict(adv=adv.cpu().numpy(), ret=ret.cpu().numpy(), logp=logp.cpu().numpy(),
-                lse=lse.cpu().numpy(), g=g.cpu().numpy(), lt=lt.cpu().numpy(), dx=dx,
-                stats=stats_all)
+    return dict(logp=logp.cpu().numpy(), lse=lse.cpu().numpy(), g=g.cpu().numpy(),
+                lt=lt.cpu().numpy(), dx=dx, stats=stats_all)
 
 
 def _compare_path(case, mode, whiten=False, rows=None):
+    """S1 and S2 compared on the GPU chain; S3+S4 then run on the GPU with the ORACLE's
+    advantages (rounded to fp32, given to both sides) so each stage is compared on the
+    same inputs and S2's rounding does not compound into the S3/S4 comparison."""
     cfg = case.cfg
     # S1: bit-exact buffer and counters
     gbuf, gcnt = H.gpu_scatter(case)
@@ -59,17 +70,20 @@ def _compare_path(case, mode, whiten=False, rows=None):
     for k in obuf:
         assert np.array_equal(gb[k].view(np.uint8), obuf[k].view(np.uint8)), f"buffer.{k}"
     assert gcnt.cpu().numpy().tolist() == ocnt.tolist()
-    out = _run_gpu_path(case, mode, gbuf, whiten=whiten)
     # S2
+    adv, ret, stats, ws = _gpu_advantages(case, mode, gbuf, whiten=whiten)
     oadv = H.oracle_advantages(case, obuf, mode, whiten=whiten)
     floor = max(1e-3, float(np.sqrt(np.mean(oadv["adv"] ** 2))))
-    H.assert_close_rel(out["adv"], oadv["adv"], 1e-5, floor, "adv")
-    H.assert_close_rel(out["ret"], oadv["ret"], 1e-5, floor, "ret")
+    H.assert_close_rel(adv.cpu().numpy(), oadv["adv"], 1e-5, floor, "adv")
+    H.assert_close_rel(ret.cpu().numpy(), oadv["ret"], 1e-5, floor, "ret")
     c = oadv["counts"]
-    st = out["stats"]
+    st = stats.cpu().numpy()
     assert st[0] == c["n_valid"] and st[3] == c["n_tok"] and st[4] == c["n_stale"] and st[5] == c["n_bad"]
-    # S3+S4 on `rows` (all by default), compared chunk by chunk
-    tv = O_path.token_view(obuf, oadv["adv"], cfg.a_tok, CUR)
+    # S3+S4 on the same advantages
+    a32 = oadv["adv"].astype(np.float32)
+    adv.copy_(torch.from_numpy(a32))
+    out = _gpu_loss(case, gbuf, adv, stats, ws)
+    tv = O_path.token_view(obuf, a32.astype(np.float64), cfg.a_tok, CUR)
     rows = np.arange(len(tv["target"])) if rows is None else rows
     refs = []
     for s in range(0, len(rows), 2048):
