@@ -36,8 +36,8 @@ UNIT = "env-steps/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="libero_spatial_oft", choices=sorted(synth.CONFIGS))
     ap.add_argument("--envs-per-gpu", type=int, default=None)
@@ -83,6 +83,10 @@ class ClockSampler:
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.p = None
+            return
+        t = time.time()     # do not start timing before the sampler is producing lines
+        while time.time() - t < 5.0 and os.path.getsize(self.f.name) == 0:
+            time.sleep(0.02)
 
     def stop(self):
         if self.p is None:
@@ -90,17 +94,19 @@ class ClockSampler:
         self.p.terminate()
         self.p.wait()
         self.f.flush()
-        rows = [l.split(",") for l in open(self.f.name).read().splitlines() if l.strip()]
+        rows = [[c.strip() for c in l.split(",")] for l in open(self.f.name).read().splitlines()
+                if l.strip()]
         os.unlink(self.f.name)
         if not rows:
             return None
-        sm = [float(r[1]) for r in rows]
-        mx = max(float(r[2]) for r in rows)
+        num = lambda v: float(v) if v.replace(".", "", 1).isdigit() else 0.0  # noqa: E731
+        sm = [num(r[1]) for r in rows]
+        mx = max(num(r[2]) for r in rows)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].strip() == "Active"})
         load = [s for s in sm if s > 0.5 * mx] or sm
         return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows)}
+                "samples": len(rows), "power_w_max": max(num(r[3]) for r in rows)}
 
 
 # --------------------------------------------------------------------------------------

@@ -85,22 +85,38 @@ __device__ __forceinline__ void block_add_counters(long long cnt[4], int64_t* co
   }
 }
 
-// M <= 1024: claim + write in one CTA
+// M <= 1024: claim + write in one CTA. Winners are flagged in shared memory after the
+// claims; the payload copy is element-parallel over all (record, token) pairs.
 __global__ void __launch_bounds__(1024) scatter_fused_kernel(ScatterArgs a) {
+  __shared__ long long s_slot[1024];  // winner's slot, -1 if the record does not win
   const int i = threadIdx.x;
   const int M = a.rec.n_rec;
   long long cnt[4] = {0, 0, 0, 0};
-  if (i < M) (void)claim_one(a, i, cnt);
-  __syncthreads();  // all claims (device-scope atomics) issued by this CTA are done
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int r = warp; r < M; r += nw) {
-    const int e = a.rec.env_id[r], t = a.rec.step[r], v = a.rec.version[r];
-    if (e < 0 || e >= a.buf.n_env || t < 0 || t >= a.buf.t_steps || v < 0 || v > a.cur_version)
-      continue;
-    const int64_t slot = int64_t(e) * a.buf.t_steps + t;
-    const uint64_t key = (uint64_t(uint32_t(v)) << kVersionShift) | (a.seq_base + uint64_t(r));
-    if (__ldcg(reinterpret_cast<const unsigned long long*>(a.buf.slot_key + slot)) == key)
-      write_payload(a, r, slot, lane);
+  Claim c{0, 0, 0};
+  if (i < M) c = claim_one(a, i, cnt);
+  __syncthreads();  // all claims (device-scope atomics) of this CTA are done
+  if (i < M) {
+    const bool win =
+        c.valid && __ldcg(reinterpret_cast<const unsigned long long*>(a.buf.slot_key + c.slot)) == c.key;
+    s_slot[i] = win ? c.slot : -1;
+    if (win) {
+      a.buf.reward[c.slot] = a.rec.reward[i];
+      a.buf.done[c.slot] = a.rec.done[i];
+      a.buf.value[c.slot] = a.rec.value[i];
+      a.buf.version[c.slot] = a.rec.version[i];
+    }
+  }
+  __syncthreads();
+  const int A = a.buf.a_tok;
+  const int n = M * A;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const int r = j / A;
+    const long long slot = s_slot[r];
+    if (slot >= 0) {
+      const long long d = slot * A + (j - r * A);
+      a.buf.tokens[d] = a.rec.tokens[j];
+      a.buf.logp_behav[d] = a.rec.logp_behav[j];
+    }
   }
   block_add_counters(cnt, a.counters);
 }
@@ -134,8 +150,10 @@ cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s) {
   const int M = a.rec.n_rec;
   if (M <= 0) return cudaSuccess;
   if (M <= 1024) {
-    int threads = ((M + 31) / 32) * 32;
-    if (threads < 64) threads = 64;
+    const int64_t work = int64_t(M) * a.buf.a_tok;
+    int threads = work > 8192 ? 1024 : 256;
+    const int need = ((M + 31) / 32) * 32;
+    if (threads < need) threads = need;
     scatter_fused_kernel<<<1, threads, 0, s>>>(a);
     return cudaGetLastError();
   }

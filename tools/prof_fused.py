@@ -1,0 +1,75 @@
+"""Time (and serve as the ncu target for) one rlvla_logprob_fwd_bwd mode at the
+LIBERO-Spatial OFT shape: 229,376 rows x 32000 bf16 (14.7 GB) on one GPU.
+
+  python tools/prof_fused.py [--mode fused|fwd|bwd] [--iters N] [--rows R]
+
+The first launch is a warm-up (ncu: -s 1 -c 1 captures the second)."""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2602_05765_b200 as P  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--mode", default="fused", choices=["fused", "fwd", "bwd"])
+    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--rows", type=int, default=229376)
+    ap.add_argument("--vocab", type=int, default=32000)
+    ap.add_argument("--A", type=int, default=56)
+    a = ap.parse_args()
+    R, V, A = a.rows, a.vocab, a.A
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(0)
+    x = torch.empty(R, V, dtype=torch.bfloat16, device=dev)
+    for s in range(0, R, 16384):
+        n = min(16384, R - s)
+        x[s:s + n] = (torch.randn(n, V, generator=g, device=dev) * 1.5).to(torch.bfloat16)
+    t = torch.randint(V - 256, V, (R,), generator=g, device=dev, dtype=torch.int32)
+    dx = torch.empty_like(x)
+    logp = torch.empty(R, device=dev)
+    lse = torch.empty(R, device=dev)
+    S = R // A
+    lb = (-11.0 + 0.1 * torch.randn(R, generator=g, device=dev)).contiguous()
+    adv = torch.randn(S, generator=g, device=dev)
+    ver = torch.full((S,), 100, dtype=torch.int32, device=dev)
+    key = torch.ones(S, dtype=torch.int64, device=dev)
+    stats = torch.zeros(16, dtype=torch.float64, device=dev)
+    ws = P.workspace(1)
+    fa = P.ppo_args(logp_behav=lb, adv=adv, version=ver, slot_key=key, a_tok=A, cur_version=100,
+                    tok_denominator=float(R))
+    gl = torch.randn(R, generator=g, device=dev) * 1e-4
+
+    def call():
+        if a.mode == "fused":
+            P.rlvla_logprob_fwd_bwd(x, t, logp=logp, fused=fa, dlogits=dx, stats=stats, ws=ws)
+        elif a.mode == "fwd":
+            P.rlvla_logprob_fwd_bwd(x, t, logp=logp, lse=lse)
+        else:
+            P.rlvla_logprob_fwd_bwd(x, t, lse=lse, grad_logp=gl, dlogits=dx)
+
+    if a.mode == "bwd":
+        P.rlvla_logprob_fwd_bwd(x, t, logp=logp, lse=lse)
+    call()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.iters + 1)]
+    ev[0].record()
+    for i in range(a.iters):
+        call()
+        ev[i + 1].record()
+    torch.cuda.synchronize()
+    ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(a.iters)]
+    rw = {"fused": 2 * V * 2 + 12, "fwd": 2 * V + 12, "bwd": 2 * V * 2 + 12}[a.mode]
+    byt = R * rw
+    avg = sum(ms) / len(ms)
+    print(json.dumps({"mode": a.mode, "rows": R, "vocab": V, "ms_avg": avg, "ms_min": min(ms),
+                      "GBps_avg": byt / avg / 1e6, "GBps_best": byt / min(ms) / 1e6}))
+
+
+if __name__ == "__main__":
+    main()
