@@ -252,6 +252,8 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     ms, k_avg, e2e_ms = vals.tolist()
+    if args.no_e2e:
+        e2e_ms = None
     units_per_step = E * cfg.n_es        # env steps of all ranks (Eq. (2) unit)
     value = units_per_step * args.steps / (ms / 1e3)
     S = E_r * T

@@ -126,10 +126,24 @@ __device__ __forceinline__ double resolve_pc(const Lp& p, PpoConst& pc) {
 }
 
 // =====================================================================================
-// K6/K5/K7 for bf16 rows up to 32768: TMA-staged persistent kernel
+// K6/K5/K7 for bf16 rows up to 32768: TMA-staged persistent kernel, two row groups
 // =====================================================================================
+// One 1024-thread CTA per SM, split into two independent 512-thread groups; group g
+// processes the CTA's rows k = g, g+2, ... Rows live in a ring of nst SMEM stages filled
+// by the TMA engine (1-D bulk copies, mbarrier tx-count completion); row k uses stage
+// k % nst. Per row a group makes three passes over the SMEM copy:
+//   A  max over its 16-byte vectors (packed bf16x2 max, no MUFU)
+//   B  e = 2^{(x - m_warp) log2e} (one ex2), sum and entropy partials per warp
+//   -- named barrier; warp 0 combines the 16 warp partials, runs the per-row epilogue
+//      (lse, logp, H, PPO g, stats) and publishes the row scalars; named barrier --
+//   C  dx = -g/S * 2^{(x - M) log2e} (second ex2), packed to bf16, 128-bit stores
+// then releases the stage by issuing the TMA for row k + nst into it. While one group
+// sits in its latency-bound combine/epilogue the other streams, so the SM never idles
+// at a CTA-wide barrier; nothing row-sized is kept in registers (no spills).
 constexpr int kCtaThreads = 1024;
-constexpr int kVecPerThread = 4;  // 4 x (8 bf16) per thread -> V <= 32768
+constexpr int kGroupThreads = 512;
+constexpr int kGroupWarps = kGroupThreads / 32;
+constexpr int kVecPerThread = 8;  // 8 x (8 bf16) per group thread -> V <= 32768
 constexpr int kMaxStages = 4;
 
 struct __align__(16) StageMeta {
@@ -142,12 +156,19 @@ struct __align__(16) StageMeta {
   uint64_t pad2;
 };
 
+struct __align__(16) RowScalars {
+  float mL;      // M * log2e (pass C exponent offset)
+  float kscale;  // -g / S_tot
+  float ga;      // dx at the target column: g * S_rest / S_tot
+  float g;
+};
+
 template <int MODE>
-__device__ __forceinline__ void issue_row(const Lp& p, int64_t r, uint8_t* dst, StageMeta* m,
+__device__ __forceinline__ void issue_row(const Lp& p, int r, uint8_t* dst, StageMeta* m,
                                           uint64_t* bar, uint32_t row_bytes, uint64_t pol) {
   cp_async4(&m->a, p.target + r);
   if (MODE == MODE_FUSED) {
-    const int64_t s = r / p.A;
+    const int s = r / p.A;
     cp_async4(&m->lpb, p.lpb + r);
     if (p.lpp) cp_async4(&m->lpp, p.lpp + r);
     cp_async4(&m->adv, p.adv + s);
@@ -159,7 +180,11 @@ __device__ __forceinline__ void issue_row(const Lp& p, int64_t r, uint8_t* dst, 
   }
   cp_async_arrive_noinc(bar);
   mbar_arrive_expect_tx(bar, row_bytes);
-  bulk_g2s(dst, static_cast<const __nv_bfloat16*>(p.x) + r * p.ld, row_bytes, bar, pol);
+  bulk_g2s(dst, static_cast<const __nv_bfloat16*>(p.x) + int64_t(r) * p.ld, row_bytes, bar, pol);
+}
+
+__device__ __forceinline__ void group_sync(int g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(kGroupThreads) : "memory");
 }
 
 template <int MODE>
@@ -169,15 +194,18 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
   uint8_t* rowbuf = smem;
   StageMeta* meta = reinterpret_cast<StageMeta*>(smem + size_t(nstages) * stage_bytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(meta + kMaxStages);
-  float4* red = reinterpret_cast<float4*>(full + kMaxStages);  // [2][32]
-  double* sacc = reinterpret_cast<double*>(red + 64);           // [16]
+  float4* red = reinterpret_cast<float4*>(full + kMaxStages);           // [2 parity][2 grp][16]
+  RowScalars* rsc = reinterpret_cast<RowScalars*>(red + 4 * kGroupWarps);  // [2]
+  double* gacc = reinterpret_cast<double*>(rsc + 2);                     // [2][16]
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int grp = tid / kGroupThreads, gt = tid % kGroupThreads, gw = gt >> 5;
   const int V = p.V;
   const int nvec = V >> 3;
   const uint32_t row_bytes = uint32_t(V) * 2u;
-  const int64_t first = blockIdx.x, stride = gridDim.x;
-  const int64_t nrow = p.rows > first ? (p.rows - first + stride - 1) / stride : 0;
+  const int first = blockIdx.x, stride = gridDim.x;
+  const int rows = int(p.rows);
+  const int nrow = rows > first ? (rows - first + stride - 1) / stride : 0;
   const bool want_stats = p.stats != nullptr && MODE != MODE_BWD;
   const float L2E = kLog2e;
   PpoConst pc;
@@ -187,171 +215,173 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     for (int s = 0; s < nstages; ++s) mbar_init(&full[s], 2);
     fence_mbar_init();
   }
-  if (tid < 16) sacc[tid] = 0.0;
+  if (tid < 32) gacc[tid] = 0.0;
   __syncthreads();
-  uint64_t pol = 0;
+  uint64_t pol = policy_evict_first();
   if (tid == 0) {
-    pol = policy_evict_first();
-    const int64_t pre = nrow < nstages ? nrow : nstages;
-    for (int64_t k = 0; k < pre; ++k)
-      issue_row<MODE>(p, first + k * stride, rowbuf + k * stage_bytes, &meta[k], &full[k],
+    const int pre = nrow < nstages ? nrow : nstages;
+    for (int k = 0; k < pre; ++k)
+      issue_row<MODE>(p, first + k * stride, rowbuf + size_t(k) * stage_bytes, &meta[k], &full[k],
                       row_bytes, pol);
   }
 
-  for (int64_t k = 0; k < nrow; ++k) {
-    const int st = int(k % nstages);
+  for (int k = grp; k < nrow; k += 2) {
+    const int st = k % nstages;
     const uint32_t ph = uint32_t((k / nstages) & 1);
-    const int64_t r = first + k * stride;
+    const int r = first + k * stride;
+    // The previous use of this stage (row k - nstages) may belong to the other group and
+    // still be in flight; a parity wait is only meaningful once that phase completed.
+    if (k >= nstages) mbar_wait(&full[st], ph ^ 1u);
     mbar_wait(&full[st], ph);
     const uint8_t* row = rowbuf + size_t(st) * stage_bytes;
     const uint4* rv = reinterpret_cast<const uint4*>(row);
     const StageMeta* mt = &meta[st];
     const int a = mt->a;
-    float lpb = 0.f, lpp = 0.f, advv = 0.f, lse_in = 0.f, g_in = 0.f;
-    int ver = 0;
-    uint64_t key = 1;
-    if (MODE == MODE_FUSED) {
-      lpb = mt->lpb;
-      if (p.lpp) lpp = mt->lpp;
-      advv = mt->adv;
-      ver = mt->ver;
-      key = mt->key;
-    } else if (MODE == MODE_BWD) {
-      lse_in = mt->lse_in;
-      g_in = mt->g_in;
-    }
     const bool tgt_ok = unsigned(a) < unsigned(V);
-    const float xa = tgt_ok ? bf_lo(uint32_t(reinterpret_cast<const uint16_t*>(row)[a])) : 0.f;
     const int va = tgt_ok ? (a >> 3) : -1;
+    // warp partials double-buffered by row parity: rows k and k+2 of a group never share
+    float4* gred = red + (((k >> 1) & 1) * 2 + grp) * kGroupWarps;
+    float g = 0.f, kscale = 0.f, ga = 0.f, mL = 0.f;
 
-    uint4 v[kVecPerThread];
-#pragma unroll
-    for (int i = 0; i < kVecPerThread; ++i) {
-      const int idx = tid + i * kCtaThreads;
-      v[i] = idx < nvec ? rv[idx] : make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);
-    }
-
-    float e[kVecPerThread * 8];
-    float mws = 0.f;
-    const int buf = int(k & 1);
     if (MODE != MODE_BWD) {
+      // ---- pass A: thread max -> warp max (packed bf16x2 max, exact) ----------------
       uint32_t mm = 0xff80ff80u;
 #pragma unroll
       for (int i = 0; i < kVecPerThread; ++i) {
-        mm = bmax2(mm, v[i].x);
-        mm = bmax2(mm, v[i].y);
-        mm = bmax2(mm, v[i].z);
-        mm = bmax2(mm, v[i].w);
+        const int idx = gt + i * kGroupThreads;
+        if (idx < nvec) {
+          const uint4 w = rv[idx];
+          mm = bmax2(bmax2(mm, w.x), bmax2(w.y, bmax2(w.z, w.w)));
+        }
       }
       const float mw = warp_max(fmaxf(bf_lo(mm), bf_hi(mm)));
-      mws = (mw == -INFINITY) ? 0.f : mw;
-      const float nmL = -mws * L2E;
+      const float nmL = (mw == -INFINITY) ? 0.f : -mw * L2E;
+      // ---- pass B: e = 2^(t), t = (x - m_warp) log2e; s = sum e, et = sum e t ------
       float s = 0.f, et = 0.f;
 #pragma unroll
       for (int i = 0; i < kVecPerThread; ++i) {
-        const uint32_t w4[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+        const int idx = gt + i * kGroupThreads;
+        if (idx < nvec) {
+          const uint4 w = rv[idx];
+          const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
+          float vs = 0.f, vet = 0.f;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float t0 = fmaf(bf_lo(w4[q]), L2E, nmL);
-          const float t1 = fmaf(bf_hi(w4[q]), L2E, nmL);
-          const float e0 = ex2(t0), e1 = ex2(t1);
-          e[i * 8 + 2 * q] = e0;
-          e[i * 8 + 2 * q + 1] = e1;
-          s += e0 + e1;
-          et = fmaf(e0, fmaxf(t0, -256.f), et);
-          et = fmaf(e1, fmaxf(t1, -256.f), et);
-        }
-      }
-      if (va >= 0 && (va & (kCtaThreads - 1)) == tid) {
-        // owner of the target column: recompute its partial sums without the target so
-        // that 1 - p_a = S_rest / S keeps full relative precision near saturation
-        s = 0.f;
-        et = 0.f;
-        const uint16_t* rh = reinterpret_cast<const uint16_t*>(row);
-        for (int i = 0; i < kVecPerThread; ++i) {
-          const int idx = tid + i * kCtaThreads;
-          if (idx >= nvec) break;
-          for (int j = 0; j < 8; ++j) {
-            if (idx * 8 + j == a) continue;
-            const float t = fmaf(bf_lo(uint32_t(rh[idx * 8 + j])), L2E, nmL);
-            const float ee = ex2(t);
-            s += ee;
-            et = fmaf(ee, fmaxf(t, -256.f), et);
+          for (int q = 0; q < 4; ++q) {
+            const float t0 = fmaf(bf_lo(w4[q]), L2E, nmL);
+            const float t1 = fmaf(bf_hi(w4[q]), L2E, nmL);
+            const float e0 = ex2(t0), e1 = ex2(t1);
+            vs += e0 + e1;
+            vet = fmaf(e0, fmaxf(t0, -256.f), vet);
+            vet = fmaf(e1, fmaxf(t1, -256.f), vet);
           }
+          if (idx == va) {
+            // the target column is excluded from the sums so that 1 - p_a = S_rest/S
+            // keeps full relative precision near saturation; recompute this vector
+            vs = 0.f;
+            vet = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if (j == (a & 7)) continue;
+              const float t = fmaf(j & 1 ? bf_hi(w4[j >> 1]) : bf_lo(w4[j >> 1]), L2E, nmL);
+              const float ee = ex2(t);
+              vs += ee;
+              vet = fmaf(ee, fmaxf(t, -256.f), vet);
+            }
+          }
+          s += vs;
+          et += vet;
         }
       }
       s = warp_sum(s);
       et = warp_sum(et);
-      if (lane == 0) red[buf * 32 + warp] = make_float4(mw, s, et, 0.f);
-    }
-    __syncthreads();  // stage `st` fully consumed; warp partials visible
-    if (tid == 0 && k + nstages < nrow) {
-      fence_proxy_async();
-      issue_row<MODE>(p, first + (k + nstages) * stride, rowbuf + size_t(st) * stage_bytes,
-                      &meta[st], &full[st], row_bytes, pol);
-    }
-
-    float g, kscale = 0.f, ga = 0.f, lse_row;
-    if (MODE != MODE_BWD) {
-      const float4 q = red[buf * 32 + lane];
-      const float M = warp_max(q.x);
-      const float sc = ex2((q.x - M) * L2E);
-      const float Srest = warp_sum(q.y * sc);
-      const float mq = (q.x == -INFINITY) ? 0.f : q.x;
-      const float Cw = sc * (q.z + (mq - M) * L2E * q.y);
-      const float Csum = warp_sum(Cw);
-      const float ta = (xa - M) * L2E;
-      const float ea = tgt_ok ? ex2(ta) : 0.f;
-      const float Stot = Srest + ea;
-      const float lnS = __logf(Stot);
-      lse_row = M + lnS;
-      const float logp = (xa - M) - lnS;
-      const float Ctot = Csum + (tgt_ok ? ea * fmaxf(ta, -256.f) : 0.f);
-      const float H = lnS - Ctot / (L2E * Stot);
-      g = finish_row<MODE>(p, pc, r, a, lse_row, logp, H, lpb, lpp, advv, ver, key, tid == 0,
-                           want_stats ? sacc : nullptr);
-      const float invS = 1.f / Stot;
-      const float cown = ex2((mws - M) * L2E);
-      kscale = -g * cown * invS;
-      ga = g * Srest * invS;  // dx at the target column: g (1 - p_a)
+      if (lane == 0) gred[gw] = make_float4(mw, s, et, 0.f);
+      // warp 0 needs x_a and the row metadata; read them before the stage can be refilled
+      float xa = 0.f, lpb = 0.f, lpp = 0.f, advv = 0.f;
+      int ver = 0;
+      uint64_t key = 1;
+      if (gw == 0) {
+        xa = tgt_ok ? bf_lo(uint32_t(reinterpret_cast<const uint16_t*>(row)[a])) : 0.f;
+        if (MODE == MODE_FUSED) {
+          lpb = mt->lpb;
+          if (p.lpp) lpp = mt->lpp;
+          advv = mt->adv;
+          ver = mt->ver;
+          key = mt->key;
+        }
+      }
+      group_sync(grp);  // #1: warp partials visible; stage no longer read in FWD mode
+      const bool has_c = (MODE == MODE_FUSED) && p.dx != nullptr;
+      if (!has_c && gt == 0 && k + nstages < nrow) {
+        fence_proxy_async();
+        issue_row<MODE>(p, first + (k + nstages) * stride, rowbuf + size_t(st) * stage_bytes,
+                        &meta[st], &full[st], row_bytes, pol);
+      }
+      if (gw == 0) {
+        // ---- combine 16 warp partials, per-row epilogue (one warp) ------------------
+        const float4 q = lane < kGroupWarps ? gred[lane] : make_float4(-INFINITY, 0.f, 0.f, 0.f);
+        const float M = warp_max(q.x);
+        const float sc = lane < kGroupWarps ? ex2((q.x - M) * L2E) : 0.f;
+        const float Srest = warp_sum(q.y * sc);
+        const float mq = (q.x == -INFINITY) ? 0.f : q.x;
+        const float Csum = warp_sum(lane < kGroupWarps ? sc * (q.z + (mq - M) * L2E * q.y) : 0.f);
+        const float ta = (xa - M) * L2E;
+        const float ea = tgt_ok ? ex2(ta) : 0.f;
+        const float Stot = Srest + ea;
+        const float lnS = __logf(Stot);
+        const float lse_row = M + lnS;
+        const float logp = (xa - M) - lnS;
+        const float invS = __fdividef(1.f, Stot);
+        const float Ctot = Csum + (tgt_ok ? ea * fmaxf(ta, -256.f) : 0.f);
+        const float H = lnS - Ctot * invS * kLn2;
+        g = finish_row<MODE>(p, pc, r, a, lse_row, logp, H, lpb, lpp, advv, ver, key, lane == 0,
+                             want_stats ? gacc + grp * 16 : nullptr);
+        if (lane == 0 && has_c) {
+          RowScalars rs;
+          rs.mL = (M == -INFINITY) ? 0.f : M * L2E;
+          rs.kscale = -g * invS;
+          rs.ga = g * Srest * invS;
+          rs.g = g;
+          rsc[grp] = rs;
+        }
+      }
+      if (!has_c) continue;
+      group_sync(grp);  // #2: row scalars published
+      const RowScalars rs = rsc[grp];
+      g = rs.g;
+      kscale = rs.kscale;
+      ga = rs.ga;
+      mL = rs.mL;
     } else {
-      g = tgt_ok ? g_in : 0.f;
-      lse_row = lse_in;
+      g = tgt_ok ? mt->g_in : 0.f;
+      mL = mt->lse_in * L2E;
+      kscale = -g;
     }
 
-    if (p.dx != nullptr && MODE != MODE_FWD) {
-      __nv_bfloat16* drow = static_cast<__nv_bfloat16*>(p.dx) + r * p.ld;
-      const float nlL = -lse_row * L2E;
+    // ---- pass C: dlogits (masked / clipped rows get exact zeros) ---------------------
+    {
+      __nv_bfloat16* drow = static_cast<__nv_bfloat16*>(p.dx) + int64_t(r) * p.ld;
+      const float nmL = -mL;
 #pragma unroll
       for (int i = 0; i < kVecPerThread; ++i) {
-        const int idx = tid + i * kCtaThreads;
+        const int idx = gt + i * kGroupThreads;
         if (idx < nvec) {
           uint4 o = make_uint4(0u, 0u, 0u, 0u);
           if (g != 0.f) {
-            float d[8];
-            if (MODE == MODE_BWD) {
-              const uint32_t w4[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+            const uint4 w = rv[idx];
+            const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
+            uint32_t* ow = &o.x;
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                d[2 * q] = -g * ex2(fmaf(bf_lo(w4[q]), L2E, nlL));
-                d[2 * q + 1] = -g * ex2(fmaf(bf_hi(w4[q]), L2E, nlL));
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 8; ++j) d[j] = kscale * e[i * 8 + j];
-            }
-            o.x = pack_bf16x2(d[0], d[1]);
-            o.y = pack_bf16x2(d[2], d[3]);
-            o.z = pack_bf16x2(d[4], d[5]);
-            o.w = pack_bf16x2(d[6], d[7]);
+            for (int q = 0; q < 4; ++q)
+              ow[q] = pack_bf16x2(kscale * ex2(fmaf(bf_lo(w4[q]), L2E, nmL)),
+                                  kscale * ex2(fmaf(bf_hi(w4[q]), L2E, nmL)));
             if (idx == va) {
-              // target column: g (1 - p_a)
               float dv;
-              if (MODE == MODE_BWD) dv = -g * expm1f(xa - lse_row);
-              else dv = ga;
+              if (MODE == MODE_BWD)
+                dv = -g * expm1f(bf_lo(uint32_t(reinterpret_cast<const uint16_t*>(row)[a])) - mt->lse_in);
+              else
+                dv = ga;
               const uint32_t hb = uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(dv)));
               const int qd = (a & 7) >> 1, hf = a & 1;
-              uint32_t* ow = &o.x;
 #pragma unroll
               for (int z = 0; z < 4; ++z)
                 if (z == qd) ow[z] = hf ? ((ow[z] & 0x0000ffffu) | (hb << 16)) : ((ow[z] & 0xffff0000u) | hb);
@@ -361,11 +391,19 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
         }
       }
     }
+    group_sync(grp);  // #3: stage fully consumed by this group
+    if (gt == 0 && k + nstages < nrow) {
+      fence_proxy_async();
+      issue_row<MODE>(p, first + (k + nstages) * stride, rowbuf + size_t(st) * stage_bytes,
+                      &meta[st], &full[st], row_bytes, pol);
+    }
   }
 
   if (want_stats) {
     __syncthreads();
-    finish_loss_stats(sacc, p.stats, p.partials, p.ctrl, Nden);
+    if (tid < 9) gacc[tid] += gacc[16 + tid];  // fixed order: group 0 then group 1
+    __syncthreads();
+    finish_loss_stats(gacc, p.stats, p.partials, p.ctrl, Nden);
   }
 }
 
@@ -642,8 +680,9 @@ cudaError_t launch_mode(const LpArgs& a, Lp p, cudaStream_t s) {
   if (path == LP_PATH_TMA) {
     const uint32_t row_bytes = uint32_t(a.x.vocab) * 2u;
     const uint32_t stage_bytes = (row_bytes + 127u) & ~127u;
-    const size_t fixed = kMaxStages * sizeof(StageMeta) + kMaxStages * 8 + 64 * sizeof(float4) +
-                         16 * sizeof(double);
+    const size_t fixed = kMaxStages * sizeof(StageMeta) + kMaxStages * 8 +
+                         4 * kGroupWarps * sizeof(float4) + 2 * sizeof(RowScalars) +
+                         32 * sizeof(double);
     int nst = int((size_t(device_info().smem_optin) - fixed - 2048) / stage_bytes);
     if (nst > kMaxStages) nst = kMaxStages;
     if (nst < 2) return cudaErrorInvalidConfiguration;
@@ -700,7 +739,8 @@ LpPath select_lp_path(const LpArgs& a) {
   const bool aligned = (xp % 16 == 0) && (dp % 16 == 0) && (V % VW == 0) && (a.x.ld % VW == 0);
   if (!aligned) return LP_PATH_GENERIC;
   if (V <= 32 * 8 * VW && V / VW <= 256) return LP_PATH_WARP;
-  if (a.x.dtype == RLVLA_BF16 && V <= kCtaThreads * kVecPerThread * 8) return LP_PATH_TMA;
+  if (a.x.dtype == RLVLA_BF16 && V <= kGroupThreads * kVecPerThread * 8 && a.x.rows < (int64_t(1) << 31))
+    return LP_PATH_TMA;
   return LP_PATH_GENERIC;
 }
 
