@@ -113,12 +113,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// try_wait suspends in hardware for a bounded time per call; ~2^26 failed calls (many
-// seconds) means a lost transaction: trap instead of hanging the GPU.
+// try_wait suspends in hardware for a bounded time per call (~us); 2^20 failed calls
+// (seconds) means a lost transaction: trap instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t n = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if (++n > (1u << 26)) __trap();
+    if (++n > (1u << 20)) __trap();
   }
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {

@@ -151,10 +151,14 @@ struct __align__(16) StageMeta {
   float lpb, lpp, adv;
   int32_t ver;
   float lse_in, g_in;
-  int32_t pad;
+  int32_t issued_row;  // row whose load was issued into this stage (plain st.shared)
   uint64_t key;
   uint64_t pad2;
 };
+
+__device__ __forceinline__ int ld_volatile_s32(const int32_t* p) {
+  return *reinterpret_cast<const volatile int32_t*>(p);
+}
 
 struct __align__(16) RowScalars {
   float mL;      // M * log2e (pass C exponent offset)
@@ -166,6 +170,7 @@ struct __align__(16) RowScalars {
 template <int MODE>
 __device__ __forceinline__ void issue_row(const Lp& p, int r, uint8_t* dst, StageMeta* m,
                                           uint64_t* bar, uint32_t row_bytes, uint64_t pol) {
+  *reinterpret_cast<volatile int32_t*>(&m->issued_row) = r;
   cp_async4(&m->a, p.target + r);
   if (MODE == MODE_FUSED) {
     const int s = r / p.A;
@@ -216,6 +221,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     fence_mbar_init();
   }
   if (tid < 32) gacc[tid] = 0.0;
+  if (tid < kMaxStages) meta[tid].issued_row = -1;
   __syncthreads();
   uint64_t pol = policy_evict_first();
   if (tid == 0) {
@@ -230,8 +236,13 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     const uint32_t ph = uint32_t((k / nstages) & 1);
     const int r = first + k * stride;
     // The previous use of this stage (row k - nstages) may belong to the other group and
-    // still be in flight; a parity wait is only meaningful once that phase completed.
-    if (k >= nstages) mbar_wait(&full[st], ph ^ 1u);
+    // still be in flight; a parity wait only distinguishes adjacent phases, so first make
+    // sure this row's load was issued (which happens only after that use was consumed).
+    {
+      uint32_t n = 0;
+      while (ld_volatile_s32(&meta[st].issued_row) != r)
+        if (++n > (1u << 24)) __trap();
+    }
     mbar_wait(&full[st], ph);
     const uint8_t* row = rowbuf + size_t(st) * stage_bytes;
     const uint4* rv = reinterpret_cast<const uint4*>(row);
