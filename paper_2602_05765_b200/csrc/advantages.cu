@@ -25,12 +25,33 @@ __device__ __forceinline__ bool step_ok_for_loss(int valid, int ver, const rlvla
   return valid && lag >= 0 && lag <= p.max_staleness;
 }
 
+// Tokens that will carry loss (target >= 0 on filled steps with 0 <= lag <= eta): one
+// warp per decision step over the whole grid; the step's key/version and its A token
+// loads are independent, so each iteration costs one memory round trip.
+__device__ __forceinline__ long long count_loss_tokens(const AdvArgs& a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nsteps = int64_t(a.buf.n_env) * a.buf.t_steps;
+  const int A = a.buf.a_tok;
+  const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  long long c = 0;
+  for (int64_t s = gw; s < nsteps; s += nw) {
+    const bool valid = a.buf.slot_key[s] != 0ull;
+    const int lag = a.p.cur_version - a.buf.version[s];
+    const int32_t* tk = a.buf.tokens + s * A;
+    int n = 0;
+    for (int j = lane; j < A; j += 32) n += tk[j] >= 0;
+    if (valid && lag >= 0 && lag <= a.p.max_staleness) c += n;
+  }
+  return c;
+}
+
 // ------------------------------------------------------------------------------------
 // GAE pass 1: scan + per-CTA partials (n_valid, sum A, sum A^2, n_tok, n_stale, n_bad)
 // ------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) gae_scan_kernel(AdvArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int E = a.buf.n_env, T = a.buf.t_steps, Atok = a.buf.a_tok;
+  const int E = a.buf.n_env, T = a.buf.t_steps;
   const float gamma = a.p.gamma, gl = a.p.gamma * a.p.lam;
   double s_n = 0, s_a = 0, s_a2 = 0;
   long long s_tok = 0, s_stale = 0, s_bad = 0;
@@ -93,26 +114,12 @@ __global__ void __launch_bounds__(256) gae_scan_kernel(AdvArgs a) {
         s_stale += stale;
         s_bad += bad;
       }
-      const int nsteps = min(32, T - tile * 32);
-      {
-        // coalesced token count over this tile's steps (all lanes participate)
-        int c = 0;
-        const int n = nsteps * Atok;
-        const int32_t* base = a.buf.tokens + (int64_t(e) * T + tile * 32) * Atok;
-        const int trips = (n + 31) >> 5;
-        for (int k = 0; k < trips; ++k) {
-          const int j = k * 32 + lane;
-          const int s = (j < n) ? j / Atok : 0;
-          const int oks = __shfl_sync(0xffffffffu, ok, s);
-          if (j < n && oks && base[j] >= 0) ++c;
-        }
-        s_tok += c;
-      }
       carryA = __shfl_sync(0xffffffffu, Aval, 0);
       carryV = __shfl_sync(0xffffffffu, V, 0);
       carry_v = __shfl_sync(0xffffffffu, v, 0);
     }
   }
+  s_tok += count_loss_tokens(a);
   // CTA partials: warp reduce then fixed-order over warps
   __shared__ double red[kWarpsPerBlock][6];
   s_n = warp_sum_d(s_n);
@@ -146,7 +153,7 @@ __global__ void __launch_bounds__(256) gae_scan_kernel(AdvArgs a) {
 // ------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) grpo_returns_kernel(AdvArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int E = a.buf.n_env, T = a.buf.t_steps, Atok = a.buf.a_tok;
+  const int E = a.buf.n_env, T = a.buf.t_steps;
   double s_n = 0;
   long long s_tok = 0, s_stale = 0, s_bad = 0;
   const int nwarps = gridDim.x * kWarpsPerBlock;
@@ -167,23 +174,14 @@ __global__ void __launch_bounds__(256) grpo_returns_kernel(AdvArgs a) {
       if (v) R += r;
       s_n += v;
       int stale, bad;
-      const int ok = step_ok_for_loss(v, ver, a.p, &stale, &bad);
+      (void)step_ok_for_loss(v, ver, a.p, &stale, &bad);
       s_stale += stale;
       s_bad += bad;
-      const int nsteps = min(32, T - tile * 32);
-      const int n = nsteps * Atok;
-      const int32_t* base = a.buf.tokens + (int64_t(e) * T + tile * 32) * Atok;
-      const int trips = (n + 31) >> 5;
-      for (int k = 0; k < trips; ++k) {
-        const int j = k * 32 + lane;
-        const int s = (j < n) ? j / Atok : 0;
-        const int oks = __shfl_sync(0xffffffffu, ok, s);
-        if (j < n && oks && base[j] >= 0) ++s_tok;
-      }
     }
     R = warp_sum(R);  // fixed xor tree: identical for any rank count
     if (lane == 0) a.ws.r_global[a.p.env_offset + e] = R;
   }
+  s_tok += count_loss_tokens(a);
   __shared__ double red[kWarpsPerBlock][4];
   s_n = warp_sum_d(s_n);
   const double t_tok = double(warp_sum_ll(s_tok));
@@ -198,7 +196,8 @@ __global__ void __launch_bounds__(256) grpo_returns_kernel(AdvArgs a) {
   __syncthreads();
   if (threadIdx.x < 6) {
     double acc = 0;
-    const int src = threadIdx.x == 0 ? 0 : (threadIdx.x >= 3 ? threadIdx.x - 2 : -1);
+    const int tx = int(threadIdx.x);
+    const int src = tx == 0 ? 0 : (tx >= 3 ? tx - 2 : -1);  // slots 0,3,4,5 <- red 0..3
     if (src >= 0)
       for (int w = 0; w < kWarpsPerBlock; ++w) acc += red[w][src];
     a.ws.partials[size_t(blockIdx.x) * RLVLA_NSTATS + threadIdx.x] = acc;  // slots 1,2 = 0
@@ -288,10 +287,22 @@ int adv_grid(int E) {
   return g < 1 ? 1 : g;
 }
 
+// pass 1 also sweeps the E*T steps for the token count: ~2 steps per warp
+int pass1_grid(int E, int T) {
+  int g = adv_grid(E);
+  const int64_t steps = int64_t(E) * T;
+  int64_t gs = (steps + 2 * kWarpsPerBlock - 1) / (2 * kWarpsPerBlock);
+  const int cap = 2 * device_info().sm_count;
+  if (gs > cap) gs = cap;
+  if (gs > g) g = int(gs);
+  if (g > kMaxPartialBlocks) g = kMaxPartialBlocks;
+  return g;
+}
+
 }  // namespace
 
 cudaError_t launch_adv_pass1(const AdvArgs& a, cudaStream_t s) {
-  const int g = adv_grid(a.buf.n_env);
+  const int g = pass1_grid(a.buf.n_env, a.buf.t_steps);
   if (a.p.mode == RLVLA_ADV_GAE) gae_scan_kernel<<<g, 256, 0, s>>>(a);
   else grpo_returns_kernel<<<g, 256, 0, s>>>(a);
   return cudaGetLastError();

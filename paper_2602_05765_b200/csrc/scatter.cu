@@ -107,16 +107,36 @@ __global__ void __launch_bounds__(1024) scatter_fused_kernel(ScatterArgs a) {
     }
   }
   __syncthreads();
+  // element-parallel payload copy; loads of a thread's (up to) 4 elements are issued
+  // before any store so each CTA pays one memory round trip, not one per element
   const int A = a.buf.a_tok;
   const int n = M * A;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    const int r = j / A;
-    const long long slot = s_slot[r];
-    if (slot >= 0) {
-      const long long d = slot * A + (j - r * A);
-      a.buf.tokens[d] = a.rec.tokens[j];
-      a.buf.logp_behav[d] = a.rec.logp_behav[j];
+  const int32_t* __restrict__ src_t = a.rec.tokens;
+  const float* __restrict__ src_l = a.rec.logp_behav;
+  for (int base = 0; base < n; base += 4 * int(blockDim.x)) {
+    int32_t tv[4];
+    float lv[4];
+    long long dst[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = base + u * int(blockDim.x) + int(threadIdx.x);
+      dst[u] = -1;
+      if (j < n) {
+        const int r = j / A;
+        const long long slot = s_slot[r];
+        if (slot >= 0) {
+          dst[u] = slot * A + (j - r * A);
+          tv[u] = __ldg(src_t + j);
+          lv[u] = __ldg(src_l + j);
+        }
+      }
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (dst[u] >= 0) {
+        a.buf.tokens[dst[u]] = tv[u];
+        a.buf.logp_behav[dst[u]] = lv[u];
+      }
   }
   block_add_counters(cnt, a.counters);
 }
@@ -151,9 +171,11 @@ cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s) {
   if (M <= 0) return cudaSuccess;
   if (M <= 1024) {
     const int64_t work = int64_t(M) * a.buf.a_tok;
-    int threads = work > 8192 ? 1024 : 256;
+    int threads = int((work + 3) / 4 + 31) / 32 * 32;  // ~4 payload elements per thread
     const int need = ((M + 31) / 32) * 32;
     if (threads < need) threads = need;
+    if (threads < 128) threads = 128;
+    if (threads > 1024) threads = 1024;
     scatter_fused_kernel<<<1, threads, 0, s>>>(a);
     return cudaGetLastError();
   }
