@@ -1,0 +1,131 @@
+"""Multi-GPU parity of the CUDA path (run under torchrun, one rank per GPU, NCCL):
+each rank scatters the records it owns, computes GRPO (groups spanning ranks: C2
+allgather + C1 allreduce) and GAE+global whitening advantages, and the fused loss with the
+C3 allreduce, all through the C ABI with the library's NCCL communicator; the result is
+compared with the oracle on the same shard using the same sharding helpers.
+
+  torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/mgpu_parity.py
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+import paper_2602_05765_b200 as P  # noqa: E402
+from paper_2602_05765_b200 import sharding  # noqa: E402
+from oracle import advantages as O_adv  # noqa: E402
+from oracle import logprob as O_lp  # noqa: E402
+from oracle import path as O_path  # noqa: E402
+from oracle import scatter as O_sc  # noqa: E402
+from tests import harness as H  # noqa: E402
+
+CUR = synth.CUR_VERSION
+
+
+def main():
+    world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    comm = P.Comm.from_process_group(device=dev)
+    E = 16 * world
+    cfg = synth.scaled(synth.CONFIGS["tiny"], n_env=E, group_size=4, interleave_groups=True)
+    traj = synth.make_trajectories(cfg)
+    rec = synth.make_records(traj, 0, E)
+    lo, hi = sharding.env_range(E, world, rank)
+    E_r, T, A, V = hi - lo, cfg.t_steps, cfg.a_tok, cfg.vocab
+    idx, local_env = sharding.route_records(rec.env_id, E, world, rank)
+    x = synth.gen_logits(cfg, traj, 0, E).double().numpy()            # all rows (for lb)
+    rows_g = synth.record_rows(rec, cfg, E)
+    f = O_lp.log_softmax_gather(x, traj.tokens.reshape(-1))["logp"]
+    lb = (np.where(rows_g >= 0, np.nan_to_num(f)[np.maximum(rows_g, 0)], 0.0) + rec.behav_noise).astype(np.float32)
+    recd = dict(env_id=local_env, step=rec.step[idx], version=rec.version[idx],
+                reward=rec.reward[idx], done=rec.done[idx], value=rec.value[idx],
+                tokens=rec.tokens[idx], logp_behav=lb[idx])
+    # ---- oracle on this shard (host) ----------------------------------------------------
+    obuf = O_sc.new_buffer(E_r, T, A)
+    ocnt = O_sc.scatter_steps(obuf, recd, CUR, 1)
+    # ---- CUDA path ----------------------------------------------------------------------
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    batch = P.StepBatch(*(t(recd[k]) for k in ("env_id", "step", "version", "reward", "done",
+                                                 "value", "tokens", "logp_behav")))
+    buf = P.TrajectoryBuffer.allocate(E_r, T, A, device=dev)
+    cnt = torch.zeros(4, dtype=torch.int64, device=dev)
+    P.rlvla_scatter_steps(buf, batch, CUR, 1, cnt)
+    gb = H.buf_to_np(buf)
+    for k in obuf:
+        assert np.array_equal(gb[k].view(np.uint8), obuf[k].view(np.uint8)), k
+    assert cnt.cpu().numpy().tolist() == ocnt.tolist()
+    ws = P.workspace(E, device=dev)
+    gid = t(traj.group_id)
+    lv = t(traj.last_value[lo:hi])
+    valid = obuf["slot_key"] != 0
+    # GRPO with groups spanning ranks (C2 + C1)
+    adv = torch.zeros(E_r, T, device=dev)
+    ret = torch.zeros(E_r, T, device=dev)
+    st = torch.zeros(16, dtype=torch.float64, device=dev)
+    P.rlvla_advantages(buf, lv, P.adv_params("grpo", group_id=gid, group_size=4, env_offset=lo,
+                                             n_env_global=E, cur_version=CUR), adv, ret, st, ws,
+                       comm=comm)
+    R_all = [torch.zeros(E_r, dtype=torch.float64, device=dev) for _ in range(world)]
+    dist.all_gather(R_all, torch.from_numpy(O_adv.episode_return(obuf["reward"], valid)).to(dev))
+    R_glob = torch.cat(R_all).cpu().numpy()
+    a_ref = O_adv.grpo_step_adv(O_adv.grpo(R_glob, traj.group_id)[lo:hi], valid)
+    H.assert_close_rel(adv.cpu().numpy(), a_ref, 1e-5, 1e-3, "grpo adv (spanning ranks)")
+    c = O_adv.step_counts(valid, obuf["version"], obuf["tokens"], CUR, 1)
+    tot = torch.tensor([c["n_valid"], c["n_tok"], c["n_stale"], c["n_bad"]], dtype=torch.float64, device=dev)
+    dist.all_reduce(tot)
+    s = st.cpu().numpy()
+    assert (s[0], s[3], s[4], s[5]) == tuple(tot.cpu().numpy().tolist()), (s[:6], tot)
+    # GAE + global whitening (C1)
+    adv2 = torch.zeros(E_r, T, device=dev)
+    st2 = torch.zeros(16, dtype=torch.float64, device=dev)
+    P.rlvla_advantages(buf, lv, P.adv_params("gae", whiten=True, env_offset=lo, n_env_global=E,
+                                             cur_version=CUR), adv2, ret, st2, ws, comm=comm)
+    a_gae, _ = O_adv.gae(obuf["reward"], obuf["value"], obuf["done"], valid, traj.last_value[lo:hi], 0.99, 0.95)
+    ws_ = torch.tensor(O_adv.whiten_stats(a_gae, valid), dtype=torch.float64, device=dev)
+    dist.all_reduce(ws_)
+    a_w = O_adv.whiten(a_gae, valid, 1e-8, stats=tuple(ws_.cpu().numpy()))
+    H.assert_close_rel(adv2.cpu().numpy(), a_w, 1e-5, max(1e-3, float(np.sqrt(np.mean(a_w ** 2)))), "gae whitened")
+    # fused loss with global N_tok (from st) and C3
+    adv.copy_(torch.from_numpy(a_ref.astype(np.float32)))
+    xr = torch.from_numpy(x[lo * T * A:hi * T * A].astype(np.float32)).to(dev)
+    R = E_r * T * A
+    logp = torch.empty(R, device=dev)
+    g = torch.empty(R, device=dev)
+    dx = torch.empty_like(xr)
+    st3 = torch.zeros(16, dtype=torch.float64, device=dev)
+    fa = P.ppo_args(logp_behav=buf.logp_behav.view(-1), adv=adv.view(-1), version=buf.version.view(-1),
+                    slot_key=buf.slot_key.view(-1), a_tok=A, cur_version=CUR, adv_stats=st,
+                    out_grad_logp=g)
+    P.rlvla_logprob_fwd_bwd(xr, buf.tokens.view(-1), logp=logp, fused=fa, dlogits=dx, stats=st3,
+                            ws=ws, comm=comm)
+    torch.cuda.synchronize()
+    tv = O_path.token_view(obuf, a_ref.astype(np.float32).astype(np.float64), A, CUR)
+    ref = O_path.loss_and_grad(x[lo * T * A:hi * T * A], tv, n_tok=float(tot[1].item()))
+    nt = ref["ppo"]["near_tie"]
+    H.assert_close_rel(g.cpu().numpy()[~nt], ref["ppo"]["grad"][~nt], 1e-5, 1e-7, "grad (global N)")
+    rs = torch.tensor([ref["stats"][k] for k in ("loss", "n_loss_tok", "entropy_sum")],
+                      dtype=torch.float64, device=dev)
+    dist.all_reduce(rs)
+    s3 = st3.cpu().numpy()
+    rs = rs.cpu().numpy()
+    assert abs(s3[6] - rs[0]) <= 1e-5 * max(1e-3, abs(rs[0])), (s3[6], rs[0])
+    assert s3[11] == rs[1] and abs(s3[9] - rs[2]) <= 1e-5 * abs(rs[2])
+    assert s3[15] == tot[1].item()
+    dist.barrier()
+    if rank == 0:
+        print(f"MGPU PARITY OK world={world} nccl={P.rlvla_nccl_version()}", flush=True)
+    comm.destroy()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
