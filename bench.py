@@ -40,7 +40,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="libero_spatial_oft", choices=sorted(synth.CONFIGS))
-    ap.add_argument("--envs-per-gpu", type=int, default=None)
+    ap.add_argument("--envs-per-gpu", type=int, default=None,
+                    help="weak-scaling configs (libero_spatial_oft): envs per GPU")
+    ap.add_argument("--microbatch-rows", type=int, default=0,
+                    help="logit rows per fused call (Streamer micro-batch, P:88); 0 = all rows "
+                         "if they fit, else ~131072 rows of whole envs")
     ap.add_argument("--chunk", type=int, default=synth.B_MAX)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -127,25 +131,45 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     base = synth.CONFIGS[args.config]
-    E_r = args.envs_per_gpu or base.n_env
-    E = E_r * world
+    weak = base.gpus == (1,)
+    if weak:      # LIBERO-Spatial OFT: 64 envs per GPU, E grows with N (weak scaling)
+        E_r = args.envs_per_gpu or base.n_env
+        E = E_r * world
+    else:         # BJ configs quoted at a GPU count: fixed global E split over N (strong)
+        E = base.n_env
+        if E % world:
+            raise SystemExit(f"{E} envs do not split over {world} GPUs")
+        E_r = E // world
     groups_span = world > 1 and base.adv_mode == "grpo"
     cfg = synth.scaled(base, n_env=E, interleave_groups=groups_span or base.interleave_groups)
     T, A, V = cfg.t_steps, cfg.a_tok, cfg.vocab
     lo, hi = sharding.env_range(E, world, rank)
     R = E_r * T * A
+    env_rows = T * A
+    if args.microbatch_rows:
+        mb_envs = max(1, args.microbatch_rows // env_rows)
+    elif R * V * 2 * 2 <= 40e9:
+        mb_envs = E_r
+    else:
+        mb_envs = max(1, 131072 // env_rows)
+    mb_envs = min(mb_envs, E_r)
+    MB = mb_envs * env_rows                       # rows per fused call
+    mbs = [(m, min(R, m + MB)) for m in range(0, R, MB)]
     comm = P.Comm.from_process_group(device=dev) if world > 1 else None
 
     # ---- inputs (outside the timed region) -------------------------------------------
     traj = synth.make_trajectories(cfg)
     rec = synth.make_records(traj, lo, hi)
-    logits = synth.gen_logits(cfg, traj, lo, hi, device=dev)          # [R, V] bf16 in HBM
+    # the VLA forward output of one micro-batch (whole envs); with several micro-batches the
+    # buffer is reused: every fused call still reads and writes all of its rows
+    logits = synth.gen_logits(cfg, traj, lo, lo + mb_envs, device=dev)   # [MB, V] bf16 in HBM
     dlogits = torch.empty_like(logits)
     # behaviour log-probs: the rollout's forward over the same rows (our fwd kernel),
     # plus the synthetic rollout/trainer drift
     tok_rows = torch.from_numpy(traj.tokens[lo:hi].reshape(-1)).to(dev)
     lp_roll = torch.empty(R, device=dev)
-    P.rlvla_logprob_fwd_bwd(logits, tok_rows, logp=lp_roll)
+    for m0, m1 in mbs:
+        P.rlvla_logprob_fwd_bwd(logits[:m1 - m0], tok_rows[m0:m1], logp=lp_roll[m0:m1])
     rows = synth.record_rows(rec, cfg, E_r)
     rows_t = torch.from_numpy(np.where(rows >= 0, rows, 0)).to(dev)
     lb = lp_roll[rows_t] * torch.from_numpy((rows >= 0).astype(np.float32)).to(dev)
@@ -171,14 +195,21 @@ def run_ours(args):
                        group_id=gid if cfg.adv_mode == "grpo" else None,
                        group_size=cfg.group_size, env_offset=lo, n_env_global=E,
                        cur_version=synth.CUR_VERSION, max_staleness=1)
-    fa = P.ppo_args(logp_behav=buf.logp_behav.view(-1), adv=adv.view(-1),
-                    version=buf.version.view(-1), slot_key=buf.slot_key.view(-1), a_tok=A,
-                    cur_version=synth.CUR_VERSION, max_staleness=1, adv_stats=stats)
+    fas = []
+    for i, (m0, m1) in enumerate(mbs):
+        s0, s1 = m0 // A, m1 // A
+        fas.append(P.ppo_args(logp_behav=buf.logp_behav.view(-1)[m0:m1], adv=adv.view(-1)[s0:s1],
+                              version=buf.version.view(-1)[s0:s1],
+                              slot_key=buf.slot_key.view(-1)[s0:s1], a_tok=A,
+                              cur_version=synth.CUR_VERSION, max_staleness=1, adv_stats=stats,
+                              accumulate=i > 0))
+    tgt_flat = buf.tokens.view(-1)
     chunks = synth.arrival_chunks(rec.n, args.chunk)
     chunk_batches = [drec.slice(sl) for sl in chunks]
     stream = torch.cuda.current_stream()
-    ev_k0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev_k1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    nmb = len(mbs)
+    ev_k0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps * nmb)]
+    ev_k1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps * nmb)]
 
     def step(i=None):
         buf.reset()
@@ -188,14 +219,17 @@ def run_ours(args):
             P.rlvla_scatter_steps(buf, cb, synth.CUR_VERSION, seq, counters, stream=stream)
             seq += sl.stop - sl.start
         P.rlvla_advantages(buf, lv, prm, adv, ret, stats, ws, comm=comm, stream=stream)
-        if i is not None:
-            ev_k0[i].record(stream)
-        P.rlvla_logprob_fwd_bwd(logits, buf.tokens.view(-1), logp=logp, fused=fa,
-                                dlogits=dlogits, stats=lstats, ws=ws, comm=comm, stream=stream)
-        if i is not None:
-            ev_k1[i].record(stream)
+        for j, ((m0, m1), fa) in enumerate(zip(mbs, fas)):
+            if i is not None:
+                ev_k0[i * nmb + j].record(stream)
+            P.rlvla_logprob_fwd_bwd(logits[:m1 - m0], tgt_flat[m0:m1], logp=logp[m0:m1], fused=fa,
+                                    dlogits=dlogits[:m1 - m0], stats=lstats, ws=ws,
+                                    comm=comm if j == nmb - 1 else None, stream=stream)
+            if i is not None:
+                ev_k1[i * nmb + j].record(stream)
 
-    launches_per_step = len(chunks) + 2 + 1   # scatter chunks + 2 advantage kernels + fused
+    n_adv_kernels = 2 if (cfg.adv_mode == "grpo" or cfg.whiten) else 1
+    launches_per_step = len(chunks) + n_adv_kernels + nmb   # scatter chunks + advantages + fused
 
     def barrier():
         if world > 1:
@@ -218,7 +252,7 @@ def run_ours(args):
     barrier()
     clocks = clk.stop()
     ms = t0.elapsed_time(t1)
-    k_ms = [a.elapsed_time(b) for a, b in zip(ev_k0, ev_k1)]
+    k_ms = [a.elapsed_time(b) for a, b in zip(ev_k0, ev_k1)]   # one per fused launch
     st_host = lstats.cpu().numpy()
     cnt = counters.cpu().numpy()
 
@@ -256,29 +290,35 @@ def run_ours(args):
         e2e_ms = None
     units_per_step = E * cfg.n_es        # env steps of all ranks (Eq. (2) unit)
     value = units_per_step * args.steps / (ms / 1e3)
-    S = E_r * T
-    alg_bytes = R * (2 * V * 2 + 4 + 4 + 4) + S * (4 + 4 + 8)   # logits rd + dlogits wr + target, logp_behav, logp + per-step
+    # algorithmic bytes of one fused launch: logits read + dlogits write + target, logp_behav,
+    # logp (4 B each) per row + adv, version, slot_key (16 B) per decision step
+    alg_bytes_step = R * (2 * V * 2 + 4 + 4 + 4) + (R // A) * (4 + 4 + 8)
+    alg_bytes = alg_bytes_step / nmb
     achieved = alg_bytes / (k_avg / 1e3) / 1e9
     peak, peak_src = peaks()
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic_fused.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("bytes_per_launch")
+            tj = json.load(open(tp))
+            if tj.get("rows_per_launch") == MB and tj.get("vocab") == V:
+                traffic = tj.get("bytes_per_launch")
         except Exception:
             traffic = None
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": cfg.name if world == 1 else f"{base.name} x{world} (weak)",
+        "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic",
+        "config": {"workload": cfg.name if (world == 1 or not weak) else f"{base.name} x{world} (weak)",
                    "envs_per_gpu": E_r, "envs_total": E, "episode_steps": cfg.n_es,
                    "chunk": cfg.chunk, "decision_steps": T, "tokens_per_step": A, "vocab": V,
                    "rows_per_gpu": R, "records_per_gpu": rec.n, "arrival_chunk": args.chunk,
+                   "fused_calls_per_step": nmb, "rows_per_fused_call": MB,
                    "advantages": cfg.adv_mode, "group_size": cfg.group_size,
                    "groups_span_ranks": bool(groups_span),
-                   "l2": f"inputs larger than L2: {logits.numel() * 2 / 1e9:.1f} GB logits read + "
-                         "same written per step per GPU, no flush needed",
+                   "l2": f"inputs larger than L2: {R * V * 2 / 1e9:.1f} GB logits read + same "
+                         "written per step per GPU, no flush needed",
                    "parallelism": f"dp{world}"},
         "clocks": clocks,
         "e2e": None if e2e_ms is None else {
@@ -287,17 +327,20 @@ def run_ours(args):
             "note": "step records H2D from pinned memory + loss stats D2H inside the timed "
                     "region; logits are the VLA forward output produced on the device"},
         "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches_per_step": {"scatter": len(chunks), "advantages": n_adv_kernels,
+                                  "fused_logprob_ppo": nmb},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "lp_tma_kernel<FUSED> (rlvla_logprob_fwd_bwd fused)",
                      "kernel_ms": k_avg, "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
-                     "kernel_share_of_step": k_avg / (ms / args.steps)},
+                     "kernel_share_of_step": k_avg * nmb / (ms / args.steps)},
         "stats_last_step": {"loss": float(st_host[6]), "clip_frac": float(st_host[7] / max(1, st_host[11])),
                             "n_loss_tok": float(st_host[11]), "n_stale_tok": float(st_host[12]),
                             "counters": cnt.tolist()},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(cfg, traj, logits, lb_fn=None)
+        out["cpu_baseline"] = cpu_baseline(cfg, traj, logits, lb_fn=None,
+                                           n_env_sample=min(2, mb_envs))
     if rank == 0:
         print(json.dumps(out), flush=True)
     if comm is not None:

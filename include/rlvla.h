@@ -210,6 +210,11 @@ typedef struct {
   const double* adv_stats;    /*  device, from rlvla_advantages)                       */
   float* out_grad_logp;       /* [rows] optional: dLoss/dlogp_r                        */
   float* out_loss_tok;        /* [rows] optional: m_r L_r (unnormalised)               */
+  int32_t accumulate;         /* 0: overwrite stats slots 6..14 (then C3 over `comm`).  */
+                              /* 1: ADD this call's slots 6..14 to `stats` (Streamer    */
+                              /*    micro-batches, §3.3; fixed call order keeps the */
+                              /*    sum deterministic). Pass `comm` only with the last   */
+                              /*    micro-batch: its C3 then reduces the running totals. */
 } rlvla_ppo_args;
 
 /* S3 (+S4) — action-token log-probs over logit rows (P:39 action tokens; P:88 actor

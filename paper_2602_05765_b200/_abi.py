@@ -54,7 +54,7 @@ class c_ppo_args(ctypes.Structure):
                 ("cur_version", c_int32), ("max_staleness", c_int32), ("eps_low", c_float),
                 ("eps_high", c_float), ("is_cap", c_float), ("tok_denominator", c_double),
                 ("adv_stats", c_void_p), ("out_grad_logp", c_void_p),
-                ("out_loss_tok", c_void_p)]
+                ("out_loss_tok", c_void_p), ("accumulate", c_int32)]
 
 
 _SIGS = {

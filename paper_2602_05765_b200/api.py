@@ -162,11 +162,12 @@ def logits_desc(x: torch.Tensor, vocab: int | None = None) -> A.c_logits:
 
 def ppo_args(*, logp_behav, adv, version, slot_key, a_tok, cur_version, max_staleness=1,
              eps_low=0.2, eps_high=0.2, is_cap=0.0, logp_prox=None, tok_denominator=0.0,
-             adv_stats=None, out_grad_logp=None, out_loss_tok=None) -> A.c_ppo_args:
+             adv_stats=None, out_grad_logp=None, out_loss_tok=None,
+             accumulate=False) -> A.c_ppo_args:
     a = A.c_ppo_args(_ptr(logp_behav), _ptr(logp_prox), _ptr(adv), _ptr(version),
                      _ptr(slot_key), a_tok, cur_version, max_staleness, eps_low, eps_high,
                      is_cap, tok_denominator, _ptr(adv_stats), _ptr(out_grad_logp),
-                     _ptr(out_loss_tok))
+                     _ptr(out_loss_tok), int(accumulate))
     # the struct holds raw pointers: keep the tensors alive as long as the struct
     a._keep = (logp_behav, logp_prox, adv, version, slot_key, adv_stats, out_grad_logp,
                out_loss_tok)

@@ -86,6 +86,7 @@ rlvla_status check_ppo_args(const rlvla_ppo_args* f) {
   if (!(f->eps_low >= 0.f) || !(f->eps_high >= 0.f) || f->eps_low >= 1.f) return RLVLA_ERR_INVALID_ARG;
   if (!(f->tok_denominator > 0.0) && !f->adv_stats) return RLVLA_ERR_INVALID_ARG;
   if (reinterpret_cast<uintptr_t>(f->slot_key) % 8) return RLVLA_ERR_INVALID_ARG;
+  if (f->accumulate != 0 && f->accumulate != 1) return RLVLA_ERR_INVALID_ARG;
   return RLVLA_OK;
 }
 

@@ -117,13 +117,15 @@ __device__ __forceinline__ double loss_denominator(double denom, const double* a
 
 // CTA partials (9 slots) -> workspace; last CTA writes stats[6..15]
 __device__ __forceinline__ void finish_loss_stats(const double* cta_acc, double* stats,
-                                                  double* partials, unsigned* ctrl, double N) {
+                                                  double* partials, unsigned* ctrl, double N,
+                                                  int accumulate) {
   if (threadIdx.x < 9) partials[size_t(blockIdx.x) * RLVLA_NSTATS + threadIdx.x] = cta_acc[threadIdx.x];
   __shared__ double tot[9];
   if (last_block_reduce(ctrl, partials, 9, tot)) {
     if (threadIdx.x < 9) {
       double v = tot[threadIdx.x];
       if (threadIdx.x == 0) v = N > 0.0 ? v / N : 0.0;
+      if (accumulate) v += stats[RLVLA_STAT_LOSS + threadIdx.x];
       stats[RLVLA_STAT_LOSS + threadIdx.x] = v;
     }
     if (threadIdx.x == 0) stats[RLVLA_STAT_DENOM] = N;

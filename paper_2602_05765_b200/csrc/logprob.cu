@@ -49,6 +49,7 @@ struct Lp {
   const double* adv_stats;
   float* out_g;
   float* out_L;
+  int accumulate;
   // stats
   double* stats;
   double* partials;
@@ -414,7 +415,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     __syncthreads();
     if (tid < 9) gacc[tid] += gacc[16 + tid];  // fixed order: group 0 then group 1
     __syncthreads();
-    finish_loss_stats(gacc, p.stats, p.partials, p.ctrl, Nden);
+    finish_loss_stats(gacc, p.stats, p.partials, p.ctrl, Nden, p.accumulate);
   }
 }
 
@@ -541,7 +542,7 @@ __global__ void __launch_bounds__(256) lp_warp_kernel(Lp p) {
       cta[threadIdx.x] = s;
     }
     __syncthreads();
-    finish_loss_stats(cta, p.stats, p.partials, p.ctrl, Nden);
+    finish_loss_stats(cta, p.stats, p.partials, p.ctrl, Nden, p.accumulate);
   }
 }
 
@@ -642,7 +643,7 @@ __global__ void __launch_bounds__(256) lp_generic_kernel(Lp p) {
   }
   if (want_stats) {
     __syncthreads();
-    finish_loss_stats(sacc, p.stats, p.partials, p.ctrl, Nden);
+    finish_loss_stats(sacc, p.stats, p.partials, p.ctrl, Nden, p.accumulate);
   }
 }
 
@@ -676,6 +677,7 @@ Lp make_lp(const LpArgs& a) {
     p.pc.is_cap = a.f.is_cap;
     p.out_g = a.f.out_grad_logp;
     p.out_L = a.f.out_loss_tok;
+    p.accumulate = a.f.accumulate;
     p.N = a.f.tok_denominator;
     p.adv_stats = a.f.adv_stats;
   }

@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) ppo_loss_kernel(PpoArgs a, PpoConst pc0) 
     cta[threadIdx.x] = s;
   }
   __syncthreads();
-  finish_loss_stats(cta, a.stats, a.ws.partials, a.ws.ctrl + CTRL_PPO, N);
+  finish_loss_stats(cta, a.stats, a.ws.partials, a.ws.ctrl + CTRL_PPO, N, a.f.accumulate);
 }
 
 }  // namespace
