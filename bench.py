@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--chunk", type=int, default=synth.B_MAX)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--eager", action="store_true",
+                    help="launch the timed steps eagerly instead of one captured CUDA graph")
     ap.add_argument("--ref-envs", type=int, default=1, help="envs per reference-arm step")
     return ap.parse_args()
 
@@ -65,6 +67,35 @@ def peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# --------------------------------------------------------------------------------------
+# CUDA events as graph nodes: cudaEventRecordWithFlags(..., cudaEventRecordExternal) during
+# stream capture records a timing event node, so kernels stay timed inside a graph replay
+# --------------------------------------------------------------------------------------
+class Cudart:
+    def __init__(self):
+        import ctypes
+        self.c = ctypes
+        self.L = ctypes.CDLL("libcudart.so.12")
+
+    def event(self):
+        e = self.c.c_void_p()
+        assert self.L.cudaEventCreate(self.c.byref(e)) == 0
+        return e
+
+    def record(self, ev, stream_handle, external):
+        fn = self.L.cudaEventRecordWithFlags
+        r = fn(ev, self.c.c_void_p(stream_handle), self.c.c_uint(1 if external else 0))
+        assert r == 0, f"cudaEventRecordWithFlags -> {r}"
+
+    def elapsed(self, a, b):
+        ms = self.c.c_float()
+        assert self.L.cudaEventElapsedTime(self.c.byref(ms), a, b) == 0
+        return ms.value
+
+    def destroy(self, e):
+        self.L.cudaEventDestroy(e)
 
 
 # --------------------------------------------------------------------------------------
@@ -206,12 +237,15 @@ def run_ours(args):
     tgt_flat = buf.tokens.view(-1)
     chunks = synth.arrival_chunks(rec.n, args.chunk)
     chunk_batches = [drec.slice(sl) for sl in chunks]
-    stream = torch.cuda.current_stream()
     nmb = len(mbs)
-    ev_k0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps * nmb)]
-    ev_k1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps * nmb)]
+    cr = Cudart()
+    ev_k0 = [cr.event() for _ in range(args.steps * nmb)]
+    ev_k1 = [cr.event() for _ in range(args.steps * nmb)]
+    ev_t0, ev_t1 = cr.event(), cr.event()
 
-    def step(i=None):
+    def step(i=None, capturing=False):
+        stream = torch.cuda.current_stream()
+        sh = stream.cuda_stream
         buf.reset()
         counters.zero_()
         seq = 1
@@ -221,12 +255,12 @@ def run_ours(args):
         P.rlvla_advantages(buf, lv, prm, adv, ret, stats, ws, comm=comm, stream=stream)
         for j, ((m0, m1), fa) in enumerate(zip(mbs, fas)):
             if i is not None:
-                ev_k0[i * nmb + j].record(stream)
+                cr.record(ev_k0[i * nmb + j], sh, capturing)
             P.rlvla_logprob_fwd_bwd(logits[:m1 - m0], tgt_flat[m0:m1], logp=logp[m0:m1], fused=fa,
                                     dlogits=dlogits[:m1 - m0], stats=lstats, ws=ws,
                                     comm=comm if j == nmb - 1 else None, stream=stream)
             if i is not None:
-                ev_k1[i * nmb + j].record(stream)
+                cr.record(ev_k1[i * nmb + j], sh, capturing)
 
     n_adv_kernels = 2 if (cfg.adv_mode == "grpo" or cfg.whiten) else 1
     launches_per_step = len(chunks) + n_adv_kernels + nmb   # scatter chunks + advantages + fused
@@ -238,21 +272,40 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    graph = None
+    if not args.eager:
+        # the K timed steps as ONE captured graph (event nodes around every fused launch)
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                cs = torch.cuda.current_stream().cuda_stream
+                cr.record(ev_t0, cs, True)
+                for i in range(args.steps):
+                    step(i, capturing=True)
+                cr.record(ev_t1, cs, True)
+            graph.replay()                      # one untimed replay (graph upload / warm-up)
+            torch.cuda.synchronize()
+        except Exception as ex:                 # pragma: no cover - fall back to eager
+            print(f"[bench] graph capture failed ({ex}); timing eagerly", file=sys.stderr)
+            graph = None
     barrier()
     clk = ClockSampler(local)
     clk.start()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     barrier()
-    t0.record(stream)
-    for i in range(args.steps):
-        step(i)
-    t1.record(stream)
+    stream = torch.cuda.current_stream()
+    if graph is not None:
+        graph.replay()
+    else:
+        cr.record(ev_t0, stream.cuda_stream, False)
+        for i in range(args.steps):
+            step(i)
+        cr.record(ev_t1, stream.cuda_stream, False)
     torch.cuda.synchronize()
     barrier()
     clocks = clk.stop()
-    ms = t0.elapsed_time(t1)
-    k_ms = [a.elapsed_time(b) for a, b in zip(ev_k0, ev_k1)]   # one per fused launch
+    ms = cr.elapsed(ev_t0, ev_t1)
+    k_ms = [cr.elapsed(a, b) for a, b in zip(ev_k0, ev_k1)]   # one per fused launch
     st_host = lstats.cpu().numpy()
     cnt = counters.cpu().numpy()
 
@@ -273,6 +326,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        stream = torch.cuda.current_stream()
         e0.record(stream)
         for _ in range(args.steps):
             e2e_step()
@@ -315,6 +369,7 @@ def run_ours(args):
                    "chunk": cfg.chunk, "decision_steps": T, "tokens_per_step": A, "vocab": V,
                    "rows_per_gpu": R, "records_per_gpu": rec.n, "arrival_chunk": args.chunk,
                    "fused_calls_per_step": nmb, "rows_per_fused_call": MB,
+                   "launch": "one CUDA graph of the K timed steps" if graph is not None else "eager",
                    "advantages": cfg.adv_mode, "group_size": cfg.group_size,
                    "groups_span_ranks": bool(groups_span),
                    "l2": f"inputs larger than L2: {R * V * 2 / 1e9:.1f} GB logits read + same "

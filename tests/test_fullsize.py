@@ -84,7 +84,6 @@ def test_fullsize_sampled_rows_match_oracle(full):
 def test_fullsize_properties(full):
     dx = full["dx"]
     R = dx.shape[0]
-    # every row's gradient sums to ~0 (sum_j (1[j=a] - p_j) = 0): bound by V * bf16 rounding
     # every row's gradient sums to ~0 (sum_j (1[j=a] - p_j) = 0): each element carries at
     # most half a bf16 ulp (2^-9 relative) of rounding
     s = torch.zeros(R, dtype=torch.float64, device="cuda")
