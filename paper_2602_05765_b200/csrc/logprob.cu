@@ -193,6 +193,23 @@ __device__ __forceinline__ void group_sync(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(kGroupThreads) : "memory");
 }
 
+__device__ __forceinline__ void advance_stage(int& st, uint32_t& ph, int nstages) {
+  st += 2;
+  if (st >= nstages) {
+    st -= nstages;
+    ph ^= 1u;
+  }
+}
+
+// barrier #2 (row scalars published) uses its own id (3 + g) so that warp 0, which only
+// arrives on it, can never be counted into another phase of the #1/#3 barrier (1 + g)
+__device__ __forceinline__ void scalars_arrive(int g) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(g + 3), "n"(kGroupThreads) : "memory");
+}
+__device__ __forceinline__ void scalars_sync(int g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(g + 3), "n"(kGroupThreads) : "memory");
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kCtaThreads, 1)
     lp_tma_kernel(Lp p, int nstages, uint32_t stage_bytes) {
@@ -200,9 +217,10 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
   uint8_t* rowbuf = smem;
   StageMeta* meta = reinterpret_cast<StageMeta*>(smem + size_t(nstages) * stage_bytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(meta + kMaxStages);
-  float4* red = reinterpret_cast<float4*>(full + kMaxStages);           // [2 parity][2 grp][16]
+  float4* red = reinterpret_cast<float4*>(full + kMaxStages);              // [2 parity][2 grp][16]
   RowScalars* rsc = reinterpret_cast<RowScalars*>(red + 4 * kGroupWarps);  // [2]
-  double* gacc = reinterpret_cast<double*>(rsc + 2);                     // [2][16]
+  float* xa_s = reinterpret_cast<float*>(rsc + 2);                         // [2 parity][2 grp]
+  double* gacc = reinterpret_cast<double*>(xa_s + 4);                      // [2][16]
 
   const int tid = threadIdx.x, lane = tid & 31;
   const int grp = tid / kGroupThreads, gt = tid % kGroupThreads, gw = gt >> 5;
@@ -213,6 +231,10 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
   const int rows = int(p.rows);
   const int nrow = rows > first ? (rows - first + stride - 1) / stride : 0;
   const bool want_stats = p.stats != nullptr && MODE != MODE_BWD;
+  // FUSED with dlogits: pass B keeps e = 2^{(x - m_warp) log2e} in the stage as bf16 (in
+  // place of x) and pass C only rescales it -- one ex2 per element in total
+  const bool has_c = MODE == MODE_BWD || (MODE == MODE_FUSED && p.dx != nullptr);
+  const bool keep_e = MODE == MODE_FUSED && p.dx != nullptr;
   const float L2E = kLog2e;
   PpoConst pc;
   const double Nden = resolve_pc<MODE>(p, pc);
@@ -232,9 +254,11 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
                       row_bytes, pol);
   }
 
+  // stage / phase of this group's rows (row k: stage k % nstages, parity (k / nstages) & 1),
+  // advanced incrementally by k += 2 (nstages >= 2)
+  int st = grp;
+  uint32_t ph = 0;
   for (int k = grp; k < nrow; k += 2) {
-    const int st = k % nstages;
-    const uint32_t ph = uint32_t((k / nstages) & 1);
     const int r = first + k * stride;
     // The previous use of this stage (row k - nstages) may belong to the other group and
     // still be in flight; a parity wait only distinguishes adjacent phases, so first make
@@ -245,15 +269,16 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
         if (++n > (1u << 24)) __trap();
     }
     mbar_wait(&full[st], ph);
-    const uint8_t* row = rowbuf + size_t(st) * stage_bytes;
-    const uint4* rv = reinterpret_cast<const uint4*>(row);
+    uint8_t* row = rowbuf + size_t(st) * stage_bytes;
+    uint4* rv = reinterpret_cast<uint4*>(row);
     const StageMeta* mt = &meta[st];
     const int a = mt->a;
     const bool tgt_ok = unsigned(a) < unsigned(V);
     const int va = tgt_ok ? (a >> 3) : -1;
     // warp partials double-buffered by row parity: rows k and k+2 of a group never share
     float4* gred = red + (((k >> 1) & 1) * 2 + grp) * kGroupWarps;
-    float g = 0.f, kscale = 0.f, ga = 0.f, mL = 0.f;
+    float* gxa = xa_s + ((k >> 1) & 1) * 2 + grp;  // raw target logit, same double buffering
+    float g = 0.f, kscale = 0.f, ga = 0.f, mL = 0.f, mws = 0.f;
 
     if (MODE != MODE_BWD) {
       // ---- pass A: thread max -> warp max (packed bf16x2 max, exact) ----------------
@@ -267,7 +292,8 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
         }
       }
       const float mw = warp_max(fmaxf(bf_lo(mm), bf_hi(mm)));
-      const float nmL = (mw == -INFINITY) ? 0.f : -mw * L2E;
+      mws = (mw == -INFINITY) ? 0.f : mw;
+      const float nmL = -mws * L2E;
       // ---- pass B: e = 2^(t), t = (x - m_warp) log2e; s = sum e, et = sum e t ------
       float s = 0.f, et = 0.f;
 #pragma unroll
@@ -276,30 +302,38 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
         if (idx < nvec) {
           const uint4 w = rv[idx];
           const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
+          float e[8];
           float vs = 0.f, vet = 0.f;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const float t0 = fmaf(bf_lo(w4[q]), L2E, nmL);
             const float t1 = fmaf(bf_hi(w4[q]), L2E, nmL);
-            const float e0 = ex2(t0), e1 = ex2(t1);
-            vs += e0 + e1;
-            vet = fmaf(e0, fmaxf(t0, -256.f), vet);
-            vet = fmaf(e1, fmaxf(t1, -256.f), vet);
+            e[2 * q] = ex2(t0);
+            e[2 * q + 1] = ex2(t1);
+            vs += e[2 * q] + e[2 * q + 1];
+            vet = fmaf(e[2 * q], fmaxf(t0, -256.f), vet);
+            vet = fmaf(e[2 * q + 1], fmaxf(t1, -256.f), vet);
           }
           if (idx == va) {
             // the target column is excluded from the sums so that 1 - p_a = S_rest/S
             // keeps full relative precision near saturation; recompute this vector
+            const int j0 = a & 7;
+            const int h = j0 >> 1;
+            const uint32_t wa = h == 0 ? w.x : (h == 1 ? w.y : (h == 2 ? w.z : w.w));
+            *gxa = (j0 & 1) ? bf_hi(wa) : bf_lo(wa);
             vs = 0.f;
             vet = 0.f;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              if (j == (a & 7)) continue;
+              if (j == j0) continue;
               const float t = fmaf(j & 1 ? bf_hi(w4[j >> 1]) : bf_lo(w4[j >> 1]), L2E, nmL);
-              const float ee = ex2(t);
-              vs += ee;
-              vet = fmaf(ee, fmaxf(t, -256.f), vet);
+              vs += e[j];
+              vet = fmaf(e[j], fmaxf(t, -256.f), vet);
             }
           }
+          if (keep_e)
+            rv[idx] = make_uint4(pack_bf16x2(e[0], e[1]), pack_bf16x2(e[2], e[3]),
+                                 pack_bf16x2(e[4], e[5]), pack_bf16x2(e[6], e[7]));
           s += vs;
           et += vet;
         }
@@ -307,34 +341,31 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
       s = warp_sum(s);
       et = warp_sum(et);
       if (lane == 0) gred[gw] = make_float4(mw, s, et, 0.f);
-      // warp 0 needs x_a and the row metadata; read them before the stage can be refilled
-      float xa = 0.f, lpb = 0.f, lpp = 0.f, advv = 0.f;
+      if (keep_e) fence_proxy_async();  // generic smem writes before the stage's next TMA fill
+      // warp 0 needs the row metadata; read it before the stage can be refilled
+      float lpb = 0.f, lpp = 0.f, advv = 0.f;
       int ver = 0;
       uint64_t key = 1;
-      if (gw == 0) {
-        xa = tgt_ok ? bf_lo(uint32_t(reinterpret_cast<const uint16_t*>(row)[a])) : 0.f;
-        if (MODE == MODE_FUSED) {
-          lpb = mt->lpb;
-          if (p.lpp) lpp = mt->lpp;
-          advv = mt->adv;
-          ver = mt->ver;
-          key = mt->key;
-        }
+      if (gw == 0 && MODE == MODE_FUSED) {
+        lpb = mt->lpb;
+        if (p.lpp) lpp = mt->lpp;
+        advv = mt->adv;
+        ver = mt->ver;
+        key = mt->key;
       }
-      group_sync(grp);  // #1: warp partials visible; stage no longer read in FWD mode
-      const bool has_c = (MODE == MODE_FUSED) && p.dx != nullptr;
+      group_sync(grp);  // #1: warp partials + x_a visible; stage no longer read in FWD mode
       if (!has_c && gt == 0 && k + nstages < nrow) {
         fence_proxy_async();
-        issue_row<MODE>(p, first + (k + nstages) * stride, rowbuf + size_t(st) * stage_bytes,
-                        &meta[st], &full[st], row_bytes, pol);
+        issue_row<MODE>(p, first + (k + nstages) * stride, row, &meta[st], &full[st], row_bytes, pol);
       }
       if (gw == 0) {
         // ---- combine 16 warp partials, per-row epilogue (one warp) ------------------
+        const float xa = tgt_ok ? *gxa : 0.f;
         const float4 q = lane < kGroupWarps ? gred[lane] : make_float4(-INFINITY, 0.f, 0.f, 0.f);
         const float M = warp_max(q.x);
         const float sc = lane < kGroupWarps ? ex2((q.x - M) * L2E) : 0.f;
-        const float Srest = warp_sum(q.y * sc);
         const float mq = (q.x == -INFINITY) ? 0.f : q.x;
+        const float Srest = warp_sum(q.y * sc);
         const float Csum = warp_sum(lane < kGroupWarps ? sc * (q.z + (mq - M) * L2E * q.y) : 0.f);
         const float ta = (xa - M) * L2E;
         const float ea = tgt_ok ? ex2(ta) : 0.f;
@@ -345,24 +376,61 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
         const float invS = __fdividef(1.f, Stot);
         const float Ctot = Csum + (tgt_ok ? ea * fmaxf(ta, -256.f) : 0.f);
         const float H = lnS - Ctot * invS * kLn2;
-        g = finish_row<MODE>(p, pc, r, a, lse_row, logp, H, lpb, lpp, advv, ver, key, lane == 0,
-                             want_stats ? gacc + grp * 16 : nullptr);
-        if (lane == 0 && has_c) {
-          RowScalars rs;
-          rs.mL = (M == -INFINITY) ? 0.f : M * L2E;
-          rs.kscale = -g * invS;
-          rs.ga = g * Srest * invS;
-          rs.g = g;
-          rsc[grp] = rs;
+        const int stt = row_status(a, V, lse_row, logp);
+        PpoRowIn in;
+        in.tgt_status = stt;
+        in.logp = (stt == 1 || stt == 2) ? 0.f : logp;
+        in.H = H;
+        in.lpb = lpb;
+        in.lpp = lpp;
+        in.adv = advv;
+        in.ver = ver;
+        in.valid = key != 0ull;
+        RowStats rs;
+        float lt = 0.f;
+        if (MODE == MODE_FUSED) g = ppo_row(pc, in, rs, &lt);
+        else fwd_row_stats(in, rs);
+        if (has_c) {
+          if (lane == 0) {
+            RowScalars sc4;
+            sc4.mL = M;                    // pass C: per-warp scale 2^{(m_w - M) log2e}
+            sc4.kscale = -g * invS;
+            sc4.ga = g * Srest * invS;
+            sc4.g = g;
+            rsc[grp] = sc4;
+          }
+          __syncwarp();
+          scalars_arrive(grp);  // #2 (producer side): the other warps may start pass C now
         }
+        // per-row outputs and statistics, off the pass-C critical path
+        if (lane == 0) {
+          p.logp[r] = in.logp;
+          if (p.lse_out) p.lse_out[r] = lse_row;
+          if (MODE == MODE_FUSED) {
+            if (p.out_g) p.out_g[r] = g;
+            if (p.out_L) p.out_L[r] = lt;
+          }
+          if (want_stats) acc_stats(gacc + grp * 16, rs);
+        }
+      } else if (has_c) {
+        scalars_sync(grp);  // #2 (consumer side): row scalars published
       }
-      if (!has_c) continue;
-      group_sync(grp);  // #2: row scalars published
-      const RowScalars rs = rsc[grp];
-      g = rs.g;
-      kscale = rs.kscale;
-      ga = rs.ga;
-      mL = rs.mL;
+      if (!has_c) {
+        advance_stage(st, ph, nstages);
+        continue;
+      }
+      if (gw != 0) {
+        const RowScalars rs4 = rsc[grp];
+        g = rs4.g;
+        kscale = rs4.kscale;
+        ga = rs4.ga;
+        mL = rs4.mL;
+      } else {
+        const RowScalars rs4 = rsc[grp];
+        kscale = rs4.kscale;
+        ga = rs4.ga;
+        mL = rs4.mL;
+      }
     } else {
       g = tgt_ok ? mt->g_in : 0.f;
       mL = mt->lse_in * L2E;
@@ -372,6 +440,9 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     // ---- pass C: dlogits (masked / clipped rows get exact zeros) ---------------------
     {
       __nv_bfloat16* drow = static_cast<__nv_bfloat16*>(p.dx) + int64_t(r) * p.ld;
+      // FUSED: dx = kscale 2^{(m_w - M) log2e} e  (e from pass B, bf16 in SMEM)
+      // BWD:   dx = -g 2^{(x - lse) log2e}
+      const float kw = MODE == MODE_BWD ? kscale : kscale * ex2((mws - mL) * L2E);
       const float nmL = -mL;
 #pragma unroll
       for (int i = 0; i < kVecPerThread; ++i) {
@@ -382,10 +453,15 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
             const uint4 w = rv[idx];
             const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
             uint32_t* ow = &o.x;
+            if (MODE == MODE_BWD) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              ow[q] = pack_bf16x2(kscale * ex2(fmaf(bf_lo(w4[q]), L2E, nmL)),
-                                  kscale * ex2(fmaf(bf_hi(w4[q]), L2E, nmL)));
+              for (int q = 0; q < 4; ++q)
+                ow[q] = pack_bf16x2(kw * ex2(fmaf(bf_lo(w4[q]), L2E, nmL)),
+                                    kw * ex2(fmaf(bf_hi(w4[q]), L2E, nmL)));
+            } else {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) ow[q] = pack_bf16x2(kw * bf_lo(w4[q]), kw * bf_hi(w4[q]));
+            }
             if (idx == va) {
               float dv;
               if (MODE == MODE_BWD)
@@ -406,9 +482,9 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     group_sync(grp);  // #3: stage fully consumed by this group
     if (gt == 0 && k + nstages < nrow) {
       fence_proxy_async();
-      issue_row<MODE>(p, first + (k + nstages) * stride, rowbuf + size_t(st) * stage_bytes,
-                      &meta[st], &full[st], row_bytes, pol);
+      issue_row<MODE>(p, first + (k + nstages) * stride, row, &meta[st], &full[st], row_bytes, pol);
     }
+    advance_stage(st, ph, nstages);
   }
 
   if (want_stats) {
@@ -695,7 +771,7 @@ cudaError_t launch_mode(const LpArgs& a, Lp p, cudaStream_t s) {
     const uint32_t stage_bytes = (row_bytes + 127u) & ~127u;
     const size_t fixed = kMaxStages * sizeof(StageMeta) + kMaxStages * 8 +
                          4 * kGroupWarps * sizeof(float4) + 2 * sizeof(RowScalars) +
-                         32 * sizeof(double);
+                         4 * sizeof(float) + 32 * sizeof(double);
     int nst = int((size_t(device_info().smem_optin) - fixed - 2048) / stage_bytes);
     if (nst > kMaxStages) nst = kMaxStages;
     if (nst < 2) return cudaErrorInvalidConfiguration;
