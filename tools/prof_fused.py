@@ -78,7 +78,8 @@ def main():
         clip = None
     print(json.dumps({"mode": a.mode, "rows": R, "vocab": V, "ms_avg": avg, "ms_min": min(ms),
                       "clip_frac": clip,
-                      "GBps_avg": byt / avg / 1e6, "GBps_best": byt / min(ms) / 1e6}))
+                      "GBps_avg": byt / avg / 1e6, "GBps_best": byt / min(ms) / 1e6,
+                      "ms_all": [round(v, 3) for v in ms]}))
 
 
 if __name__ == "__main__":
