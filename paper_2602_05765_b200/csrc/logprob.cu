@@ -311,8 +311,17 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
             e[2 * q] = ex2(t0);
             e[2 * q + 1] = ex2(t1);
             vs += e[2 * q] + e[2 * q + 1];
-            vet = fmaf(e[2 * q], fmaxf(t0, -256.f), vet);
-            vet = fmaf(e[2 * q + 1], fmaxf(t1, -256.f), vet);
+            vet = fmaf(e[2 * q], t0, vet);
+            vet = fmaf(e[2 * q + 1], t1, vet);
+          }
+          if (isnan(vet)) {
+            // a -inf column gives e * t = 0 * -inf: redo this vector with t clamped (rare)
+            vet = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float t = fmaf(j & 1 ? bf_hi(w4[j >> 1]) : bf_lo(w4[j >> 1]), L2E, nmL);
+              vet = fmaf(e[j], fmaxf(t, -256.f), vet);
+            }
           }
           if (idx == va) {
             // the target column is excluded from the sums so that 1 - p_a = S_rest/S

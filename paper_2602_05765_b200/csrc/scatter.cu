@@ -85,12 +85,28 @@ __device__ __forceinline__ void block_add_counters(long long cnt[4], int64_t* co
   }
 }
 
-// M <= 1024: claim + write in one CTA. Winners are flagged in shared memory after the
-// claims; the payload copy is element-parallel over all (record, token) pairs.
+// M <= 1024: claim + write in one CTA. The first 4 payload elements of every thread are
+// loaded at kernel start (independent of the claim), winners are flagged in shared memory
+// after the claims, and the copy is element-parallel over all (record, token) pairs:
+// two dependent global round trips (claim, re-read key) plus the stores.
 __global__ void __launch_bounds__(1024) scatter_fused_kernel(ScatterArgs a) {
   __shared__ long long s_slot[1024];  // winner's slot, -1 if the record does not win
   const int i = threadIdx.x;
   const int M = a.rec.n_rec;
+  const int A = a.buf.a_tok;
+  const int n = M * A;
+  const int32_t* __restrict__ src_t = a.rec.tokens;
+  const float* __restrict__ src_l = a.rec.logp_behav;
+  int32_t tv[4];
+  float lv[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int j = u * int(blockDim.x) + i;
+    if (j < n) {
+      tv[u] = __ldg(src_t + j);
+      lv[u] = __ldg(src_l + j);
+    }
+  }
   long long cnt[4] = {0, 0, 0, 0};
   Claim c{0, 0, 0};
   if (i < M) c = claim_one(a, i, cnt);
@@ -107,19 +123,25 @@ __global__ void __launch_bounds__(1024) scatter_fused_kernel(ScatterArgs a) {
     }
   }
   __syncthreads();
-  // element-parallel payload copy; loads of a thread's (up to) 4 elements are issued
-  // before any store so each CTA pays one memory round trip, not one per element
-  const int A = a.buf.a_tok;
-  const int n = M * A;
-  const int32_t* __restrict__ src_t = a.rec.tokens;
-  const float* __restrict__ src_l = a.rec.logp_behav;
-  for (int base = 0; base < n; base += 4 * int(blockDim.x)) {
-    int32_t tv[4];
-    float lv[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int j = u * int(blockDim.x) + i;
+    if (j < n) {
+      const int r = j / A;
+      const long long slot = s_slot[r];
+      if (slot >= 0) {
+        const long long d = slot * A + (j - r * A);
+        a.buf.tokens[d] = tv[u];
+        a.buf.logp_behav[d] = lv[u];
+      }
+    }
+  }
+  // remaining elements (M * A > 4 * blockDim): loads batched before stores
+  for (int base = 4 * int(blockDim.x); base < n; base += 4 * int(blockDim.x)) {
     long long dst[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int j = base + u * int(blockDim.x) + int(threadIdx.x);
+      const int j = base + u * int(blockDim.x) + i;
       dst[u] = -1;
       if (j < n) {
         const int r = j / A;
