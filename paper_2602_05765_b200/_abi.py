@@ -9,7 +9,8 @@ from ctypes import POINTER, c_double, c_float, c_int32, c_int64, c_size_t, c_uin
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-LIB_PATH = os.path.join(PKG, "librlvla.so")
+# RLVLA_LIB overrides the library path (A/B timing of variant builds in tools/)
+LIB_PATH = os.environ.get("RLVLA_LIB") or os.path.join(PKG, "librlvla.so")
 HEADER = os.path.join(ROOT, "include", "rlvla.h")
 
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_NCCL, ERR_DATA = range(6)

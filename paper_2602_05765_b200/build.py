@@ -34,9 +34,9 @@ def _flags():
                    "-Xptxas", "-v"]
 
 
-def _compile(src: str) -> tuple[str, str]:
-    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-    cmd = [NVCC, "-c", src, "-o", obj] + _flags()
+def _compile(src: str, tag: str = "", defines: tuple = ()) -> tuple[str, str]:
+    obj = os.path.join(BUILD, os.path.basename(src) + tag + ".o")
+    cmd = [NVCC, "-c", src, "-o", obj] + _flags() + [f"-D{d}" for d in defines]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
@@ -52,28 +52,32 @@ def _stale(srcs) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Compile csrc/*.cu and link librlvla.so (or `out`, e.g. a variant for A/B timing)."""
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    if not force and not _stale(srcs):
+    target = out or OUT
+    if out is None and not force and not _stale(srcs):
         return OUT
     os.makedirs(BUILD, exist_ok=True)
+    tag = "" if out is None else "." + os.path.basename(out)
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        results = list(ex.map(_compile, srcs))
-    with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
+        results = list(ex.map(lambda f: _compile(f, tag, defines), srcs))
+    with open(os.path.join(BUILD, "ptxas" + tag + ".log"), "w") as f:
         for (obj, log) in results:
             f.write(f"== {obj}\n{log}\n")
     nd = nccl_dir()
-    tmp = OUT + ".tmp"
+    tmp = target + ".tmp"
     cmd = [NVCC, "-shared", "-o", tmp] + [o for o, _ in results] + ARCH + [
         "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
         "-Xlinker", "-rpath", "-Xlinker", os.path.join(nd, "lib")]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, OUT)
+    os.replace(tmp, target)
     if verbose:
         print(open(os.path.join(BUILD, "ptxas.log")).read())
-    return OUT
+    return target
 
 
 if __name__ == "__main__":

@@ -26,6 +26,11 @@ namespace {
 
 enum { MODE_FWD = 0, MODE_FUSED = 1, MODE_BWD = 2 };
 
+// build-time variants for A/B timing (tools/ab_variants.py); defaults are the product
+#ifndef RLVLA_ENTROPY_CLAMP
+#define RLVLA_ENTROPY_CLAMP 0   // 1: clamp t per element instead of the NaN-guarded redo
+#endif
+
 struct Lp {
   const void* x;
   int64_t rows;
@@ -311,10 +316,15 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
             e[2 * q] = ex2(t0);
             e[2 * q + 1] = ex2(t1);
             vs += e[2 * q] + e[2 * q + 1];
+#if RLVLA_ENTROPY_CLAMP
+            vet = fmaf(e[2 * q], fmaxf(t0, -256.f), vet);
+            vet = fmaf(e[2 * q + 1], fmaxf(t1, -256.f), vet);
+#else
             vet = fmaf(e[2 * q], t0, vet);
             vet = fmaf(e[2 * q + 1], t1, vet);
+#endif
           }
-          if (isnan(vet)) {
+          if (!RLVLA_ENTROPY_CLAMP && isnan(vet)) {
             // a -inf column gives e * t = 0 * -inf: redo this vector with t clamped (rare)
             vet = 0.f;
 #pragma unroll
