@@ -26,10 +26,9 @@ namespace {
 
 enum { MODE_FWD = 0, MODE_FUSED = 1, MODE_BWD = 2 };
 
-// build-time variants for A/B timing (tools/ab_variants.py); defaults are the product
-#ifndef RLVLA_ENTROPY_CLAMP
-#define RLVLA_ENTROPY_CLAMP 0   // 1: clamp t per element instead of the NaN-guarded redo
-#endif
+// build-time variants for A/B timing (tools/ab_variants.py); defaults are the product.
+// (Measured and rejected: a NaN-guarded per-vector redo instead of the per-element -inf
+// clamp in the entropy partial — 4% slower, the per-vector branch costs more than it saves.)
 
 struct Lp {
   const void* x;
@@ -316,22 +315,8 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
             e[2 * q] = ex2(t0);
             e[2 * q + 1] = ex2(t1);
             vs += e[2 * q] + e[2 * q + 1];
-#if RLVLA_ENTROPY_CLAMP
-            vet = fmaf(e[2 * q], fmaxf(t0, -256.f), vet);
+            vet = fmaf(e[2 * q], fmaxf(t0, -256.f), vet);      // -inf column: 0 * -256
             vet = fmaf(e[2 * q + 1], fmaxf(t1, -256.f), vet);
-#else
-            vet = fmaf(e[2 * q], t0, vet);
-            vet = fmaf(e[2 * q + 1], t1, vet);
-#endif
-          }
-          if (!RLVLA_ENTROPY_CLAMP && isnan(vet)) {
-            // a -inf column gives e * t = 0 * -inf: redo this vector with t clamped (rare)
-            vet = 0.f;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float t = fmaf(j & 1 ? bf_hi(w4[j >> 1]) : bf_lo(w4[j >> 1]), L2E, nmL);
-              vet = fmaf(e[j], fmaxf(t, -256.f), vet);
-            }
           }
           if (idx == va) {
             // the target column is excluded from the sums so that 1 - p_a = S_rest/S

@@ -12,7 +12,6 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
-    "entropy_clamp": ("RLVLA_ENTROPY_CLAMP=1",),
 }
 
 
