@@ -97,6 +97,9 @@ __global__ void __launch_bounds__(1024) scatter_fused_kernel(ScatterArgs a) {
   const int n = M * A;
   const int32_t* __restrict__ src_t = a.rec.tokens;
   const float* __restrict__ src_l = a.rec.logp_behav;
+  // Programmatic dependent launch: let the next arrival chunk's kernel start launching now;
+  // it waits (griddepcontrol.wait) before touching the buffer, so chunk order is kept.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   int32_t tv[4];
   float lv[4];
 #pragma unroll
@@ -107,6 +110,8 @@ __global__ void __launch_bounds__(1024) scatter_fused_kernel(ScatterArgs a) {
       lv[u] = __ldg(src_l + j);
     }
   }
+  // the records are inputs; the buffer may still be written by the previous chunk's kernel
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   long long cnt[4] = {0, 0, 0, 0};
   Claim c{0, 0, 0};
   if (i < M) c = claim_one(a, i, cnt);
@@ -198,8 +203,16 @@ cudaError_t launch_scatter(const ScatterArgs& a, cudaStream_t s) {
     if (threads < need) threads = need;
     if (threads < 128) threads = 128;
     if (threads > 1024) threads = 1024;
-    scatter_fused_kernel<<<1, threads, 0, s>>>(a);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(threads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, scatter_fused_kernel, a);
   }
   const int sms = device_info().sm_count;
   int blocks = (M + 255) / 256;
