@@ -83,6 +83,14 @@ __device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
   return *reinterpret_cast<uint32_t*>(&z);
 }
 
+// packed bf16x2 max that propagates NaN (HMNMX2.NAN)
+__device__ __forceinline__ uint32_t bmax2_nan(uint32_t a, uint32_t b) {
+  __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&a);
+  __nv_bfloat162 y = *reinterpret_cast<__nv_bfloat162*>(&b);
+  __nv_bfloat162 z = __hmax2_nan(x, y);
+  return *reinterpret_cast<uint32_t*>(&z);
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -27,6 +27,9 @@ namespace {
 enum { MODE_FWD = 0, MODE_FUSED = 1, MODE_BWD = 2 };
 
 // build-time variants for A/B timing (tools/ab_variants.py); defaults are the product.
+#ifndef RLVLA_PACKED_CLAMP
+#define RLVLA_PACKED_CLAMP 0  // 1: clamp -inf per bf16 pair instead of per element
+#endif
 // (Measured and rejected: a NaN-guarded per-vector redo instead of the per-element -inf
 // clamp in the entropy partial — 4% slower, the per-vector branch costs more than it saves.)
 
@@ -308,6 +311,23 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
           const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
           float e[8];
           float vs = 0.f, vet = 0.f;
+#if RLVLA_PACKED_CLAMP
+          // -inf -> -2^100 once per bf16 pair (NaN-propagating max): e = 0 and e*t = 0 for
+          // those columns without a per-element clamp; NaN and +inf pass through unchanged
+          uint32_t c4[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) c4[q] = bmax2_nan(w4[q], 0xF180F180u);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float t0 = fmaf(bf_lo(c4[q]), L2E, nmL);
+            const float t1 = fmaf(bf_hi(c4[q]), L2E, nmL);
+            e[2 * q] = ex2(t0);
+            e[2 * q + 1] = ex2(t1);
+            vs += e[2 * q] + e[2 * q + 1];
+            vet = fmaf(e[2 * q], t0, vet);
+            vet = fmaf(e[2 * q + 1], t1, vet);
+          }
+#else
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const float t0 = fmaf(bf_lo(w4[q]), L2E, nmL);
@@ -318,6 +338,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
             vet = fmaf(e[2 * q], fmaxf(t0, -256.f), vet);      // -inf column: 0 * -256
             vet = fmaf(e[2 * q + 1], fmaxf(t1, -256.f), vet);
           }
+#endif
           if (idx == va) {
             // the target column is excluded from the sums so that 1 - p_a = S_rest/S
             // keeps full relative precision near saturation; recompute this vector
