@@ -12,7 +12,7 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
-    "packed_clamp": ("RLVLA_PACKED_CLAMP=1",),
+    "element_clamp": ("RLVLA_PACKED_CLAMP=0",),
 }
 
 
