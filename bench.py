@@ -216,8 +216,8 @@ def run_ours(args):
     counters = torch.zeros(4, dtype=torch.int64, device=dev)
     adv = torch.zeros(E_r, T, device=dev)
     ret = torch.zeros(E_r, T, device=dev)
-    stats = torch.zeros(16, dtype=torch.float64, device=dev)
-    lstats = torch.zeros(16, dtype=torch.float64, device=dev)
+    stats = torch.zeros(24, dtype=torch.float64, device=dev)
+    lstats = torch.zeros(24, dtype=torch.float64, device=dev)
     logp = torch.empty(R, device=dev)
     ws = P.workspace(E, device=dev)
     lv = torch.from_numpy(traj.last_value[lo:hi]).to(dev)

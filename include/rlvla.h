@@ -63,8 +63,9 @@ typedef enum { RLVLA_F32 = 0, RLVLA_BF16 = 1 } rlvla_dtype;
 
 /* Statistics vector: double[RLVLA_NSTATS], device memory, slots below.
  * rlvla_advantages writes slots 0..5 (and allreduces them over `comm`);
- * rlvla_logprob_fwd_bwd / rlvla_ppo_loss write slots 6..15 (allreducing 6..14).
- * Each call OVERWRITES its slots (micro-batch partials are summed by the caller). */
+ * rlvla_logprob_fwd_bwd / rlvla_ppo_loss write slots 6..18 (allreducing 6..17);
+ * rlvla_value_loss writes slots 19..22 (allreducing 19..21).
+ * Each call OVERWRITES its slots unless `accumulate` is set (Streamer micro-batches). */
 enum {
   RLVLA_STAT_N_VALID_STEPS = 0, /* #filled buffer slots (slot_key != 0)               */
   RLVLA_STAT_SUM_ADV = 1,       /* GAE: sum of raw advantages over filled slots (0 GRPO)*/
@@ -72,9 +73,9 @@ enum {
   RLVLA_STAT_N_TOK = 3,         /* #tokens with target>=0 on filled steps, 0<=lag<=eta  */
   RLVLA_STAT_N_STALE_STEPS = 4, /* #filled steps with lag > eta                        */
   RLVLA_STAT_N_BAD_STEPS = 5,   /* #filled steps with lag < 0                          */
-  RLVLA_STAT_LOSS = 6,          /* sum_r m_r L_r / N_tok  (this call's share of the loss)*/
-  RLVLA_STAT_N_CLIPPED = 7,     /* #loss tokens whose surrogate gradient was clipped    */
-  RLVLA_STAT_KL_K3_SUM = 8,     /* sum_r m_r (rho - 1 - ln rho)                         */
+  RLVLA_STAT_LOSS = 6,          /* total loss share: sum_r m_r L_r / N - ent_coef sum m H / N */
+  RLVLA_STAT_N_CLIPPED = 7,     /* #loss tokens (steps, chunk ratio) whose surrogate was clipped */
+  RLVLA_STAT_KL_K3_SUM = 8,     /* sum_r m_r (rho - 1 - ln rho)  (policy vs behaviour/prox) */
   RLVLA_STAT_ENTROPY_SUM = 9,   /* sum_r m_r H_r (logits paths only; 0 in ppo_loss)     */
   RLVLA_STAT_RATIO_SUM = 10,    /* sum_r m_r rho                                        */
   RLVLA_STAT_N_LOSS_TOK = 11,   /* sum_r m_r                                            */
@@ -82,8 +83,16 @@ enum {
   RLVLA_STAT_N_BAD_TOK = 13,    /* tokens with target outside [-1,V), non-finite logp,  */
                                 /* or lag < 0 (on filled steps)                         */
   RLVLA_STAT_LOGP_SUM = 14,     /* sum_r m_r logp_r                                     */
-  RLVLA_STAT_DENOM = 15,        /* the N_tok used for the 1/N_tok normalisation         */
-  RLVLA_NSTATS = 16
+  RLVLA_STAT_KL_REF_SUM = 15,   /* sum_r m_r k3(ref), k3 = e^{lr} - lr - 1, lr = logp_ref - logp */
+  RLVLA_STAT_N_DUAL_CLIPPED = 16, /* #loss tokens on the dual-clip branch (A < 0, c A > J) */
+  RLVLA_STAT_PG_LOSS = 17,      /* clipped-surrogate part alone: sum_r m_r L_pg,r / N   */
+  RLVLA_STAT_DENOM = 18,        /* the N used for the 1/N normalisation                 */
+  RLVLA_STAT_VALUE_LOSS = 19,   /* rlvla_value_loss: sum_s m_s L_v,s / N_v              */
+  RLVLA_STAT_N_VALUE_CLIPPED = 20, /* #steps on the clipped value branch                */
+  RLVLA_STAT_N_VALUE_STEPS = 21,   /* sum_s m_s                                         */
+  RLVLA_STAT_VALUE_DENOM = 22,     /* the N_v used                                      */
+  RLVLA_STAT_RESERVED = 23,
+  RLVLA_NSTATS = 24
 };
 
 /* Scatter counters: int64[4], ADDED to by rlvla_scatter_steps (caller zeroes). */
@@ -161,15 +170,19 @@ typedef struct {
   int32_t n_env_global;      /* n_env * nranks                                           */
   /* token bookkeeping for the loss normaliser (slot RLVLA_STAT_N_TOK): */
   int32_t cur_version, max_staleness;
+  /* GAE time-limit truncation (NEXT-2, reading R23): a step with done == 2 ends the episode */
+  /* by truncation; the recursion is cut but delta bootstraps from boot_value[e*T + t]      */
+  /* (V of the true next state). NULL => done == 2 bootstraps 0 like a termination.        */
+  const float* boot_value;
 } rlvla_adv_params;
 
 /* S2 — advantages for every slot of `buf`.
  * adv, ret: device float[n_env*t_steps]. GAE: adv = A_t (whitened if p->whiten),
  * ret = A_t + V_t (raw); GRPO: adv = A_e on filled steps, ret = R_e (ret may be NULL).
  * Never-filled slots get adv = ret = 0 and cut the GAE recursion (R8).
- * GAE per env, t = T-1..0: nt_t = v_t (1 - done_t) v_{t+1} (v_T := 1);
- * delta_t = v_t (r_t + gamma nt_t V_{t+1} - V_t) with V_T = last_value[e] (NULL => 0);
- * A_t = delta_t + gamma lam nt_t A_{t+1}. Computed as a warp-parallel suffix scan of the
+ * GAE per env, t = T-1..0: nt_t = v_t [done_t == 0] v_{t+1} (v_T := 1), tr_t = [done_t == 2];
+ * delta_t = v_t (r_t + gamma (nt_t V_{t+1} + tr_t B_t) - V_t) with V_T = last_value[e]
+ * (NULL => 0), B = boot_value; A_t = delta_t + gamma lam nt_t A_{t+1}. Computed as a warp-parallel suffix scan of the
  * affine maps A -> delta_t + c_t A (fp32, fp64 statistics).
  * stats: device double[16]; slots 0..5 written and allreduced over `comm` (C1). With
  * GRPO and comm != NULL the per-env returns are allgathered (C2) first. */
@@ -210,11 +223,21 @@ typedef struct {
   const double* adv_stats;    /*  device, from rlvla_advantages)                       */
   float* out_grad_logp;       /* [rows] optional: dLoss/dlogp_r                        */
   float* out_loss_tok;        /* [rows] optional: m_r L_r (unnormalised)               */
-  int32_t accumulate;         /* 0: overwrite stats slots 6..14 (then C3 over `comm`).  */
-                              /* 1: ADD this call's slots 6..14 to `stats` (Streamer    */
+  int32_t accumulate;         /* 0: overwrite stats slots 6..18 (then C3 over `comm`).  */
+                              /* 1: ADD this call's slots 6..17 to `stats` (Streamer    */
                               /*    micro-batches, §3.3; fixed call order keeps the */
                               /*    sum deterministic). Pass `comm` only with the last   */
                               /*    micro-batch: its C3 then reduces the running totals. */
+  /* Loss variants (all paper-silent, readings R19-R21). 0 / NULL = off.   */
+  float dual_clip;            /* c > 1: for A < 0 the objective is max(J, c A) (Ye et al. */
+                              /* 2020); tokens with c A > J get no gradient             */
+  const float* logp_ref;      /* [rows] reference-policy log-probs (KL penalty), or NULL */
+  float kl_coef;              /* L_r += kl_coef k3, k3 = e^{lr} - lr - 1, lr = logp_ref - logp */
+  float ent_coef;             /* Loss -= ent_coef sum m H / N with its gradient through  */
+                              /* the logits (logits path only; 0 in rlvla_ppo_loss)     */
+  int32_t ratio_level;        /* rlvla_ppo_loss only: 0 token ratio; 1 one ratio per     */
+                              /* decision step = the action chunk's likelihood ratio    */
+                              /* exp(sum_a m (logp - logp_behav)), Loss / N_steps       */
 } rlvla_ppo_args;
 
 /* S3 (+S4) — action-token log-probs over logit rows (P:39 action tokens; P:88 actor
@@ -249,6 +272,21 @@ RLVLA_API rlvla_status rlvla_ppo_loss(const float* logp, int64_t rows, const int
                             const rlvla_ppo_args* a, float* grad_logp, float* loss_tok,
                             double* stats, void* workspace, size_t ws_bytes, rlvla_comm comm,
                             void* stream);
+
+/* S4 value head (reading R22): clipped value loss per decision step,
+ *   L_s = 0.5 max((v - R)^2, (v_old + clip(v - v_old, -clip_eps, clip_eps) - R)^2)
+ * (clip_eps <= 0 => 0.5 (v - R)^2), m_s = [slot_key != 0][0 <= lag <= max_staleness],
+ * Loss = sum m L / N_v with N_v = denominator (> 0) or the call's sum m_s (then per rank;
+ * pass an explicit global N_v with comm). grad_v[s] = dLoss/dv_s (required), loss_step
+ * optional. v_new, v_old (= buffer value), ret: float[n_steps]. stats slots 19..22 (C over
+ * comm for 19..21). */
+RLVLA_API rlvla_status rlvla_value_loss(const float* v_new, const float* v_old, const float* ret,
+                                        const uint64_t* slot_key, const int32_t* version,
+                                        int64_t n_steps, int32_t cur_version,
+                                        int32_t max_staleness, float clip_eps,
+                                        double denominator, float* grad_v, float* loss_step,
+                                        double* stats, void* workspace, size_t ws_bytes,
+                                        rlvla_comm comm, void* stream);
 
 /* Workspace bytes for calls on buffers/logits up to these sizes (host-only, no GPU). */
 RLVLA_API size_t rlvla_workspace_bytes(int64_t rows, int32_t n_env_global, int32_t t_steps);

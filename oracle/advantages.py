@@ -15,29 +15,32 @@ from __future__ import annotations
 import numpy as np
 
 
-def gae(reward, value, done, valid, last_value, gamma: float, lam: float):
-    """Per env, t = T-1 .. 0:
+def gae(reward, value, done, valid, last_value, gamma: float, lam: float, boot_value=None):
+    """Per env, t = T-1 .. 0 (truncation = NEXT-2 reading R23):
         v_t   = valid(e, t);                 v_T := 1
-        nt_t  = v_t * (1 - done_t) * v_{t+1}
+        nt_t  = v_t * [done_t == 0] * v_{t+1}
+        tr_t  = [done_t == 2]  (time-limit truncation: bootstrap B_t = boot_value, then cut)
         nV_t  = last_value[e] if t == T-1 else V_{t+1}
-        delta = v_t * (r_t + gamma * nt_t * nV_t - V_t)
+        delta = v_t * (r_t + gamma * (nt_t * nV_t + tr_t * B_t) - V_t)
         A_t   = delta + gamma * lam * nt_t * A_{t+1},   A_T = 0
         R_t   = A_t + V_t  (valid steps; 0 elsewhere)
-    Returns (adv, ret) float64 [E, T].
+    done_t = 1 is a termination (reading R7). Returns (adv, ret) float64 [E, T].
     """
     r = np.asarray(reward, np.float64)
     V = np.asarray(value, np.float64)
-    d = np.asarray(done, np.float64)
+    d = np.asarray(done, np.int64)
     v = np.asarray(valid, np.float64)
     E, T = r.shape
     lv = np.zeros(E) if last_value is None else np.asarray(last_value, np.float64)
+    B = np.zeros((E, T)) if boot_value is None else np.asarray(boot_value, np.float64)
     adv = np.zeros((E, T))
     A_next = np.zeros(E)
     for t in range(T - 1, -1, -1):
         v_next = v[:, t + 1] if t + 1 < T else np.ones(E)
         V_next = V[:, t + 1] if t + 1 < T else lv
-        nt = v[:, t] * (1.0 - d[:, t]) * v_next
-        delta = v[:, t] * (r[:, t] + gamma * nt * V_next - V[:, t])
+        nt = v[:, t] * (d[:, t] == 0) * v_next
+        tr = (d[:, t] == 2).astype(np.float64)
+        delta = v[:, t] * (r[:, t] + gamma * (nt * V_next + tr * B[:, t]) - V[:, t])
         A = delta + gamma * lam * nt * A_next
         adv[:, t] = A
         A_next = A

@@ -71,3 +71,16 @@ def log_softmax_grad(x, target, lse, g):
         dx[r, a] = g[r] * rest
     dx[g == 0] = 0.0
     return dx
+
+
+def entropy_bonus_grad(x, lse, H, coef_r):
+    """Gradient of -coef * H w.r.t. the logits (entropy bonus, NEXT-2, reading R20):
+    dH/dx_j = -p_j (log p_j + H)  =>  d(-c H)/dx_j = c p_j (log p_j + H). coef_r: [R]
+    (the per-row weight m_r beta / N_tok). -inf columns (p_j = 0) contribute 0."""
+    x = np.asarray(x, np.float64)
+    lse = np.asarray(lse, np.float64)
+    with np.errstate(invalid="ignore", over="ignore"):
+        logp_all = x - lse[:, None]
+        p = np.exp(logp_all)
+        t = np.where(p > 0, p * (logp_all + np.asarray(H, np.float64)[:, None]), 0.0)
+    return np.asarray(coef_r, np.float64)[:, None] * t

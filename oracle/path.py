@@ -61,7 +61,8 @@ def token_view(buf, adv, a_tok, cur_version):
 
 
 def loss_and_grad(logits, tv, *, eps_low=0.2, eps_high=0.2, max_staleness=1, n_tok=None,
-                  logp_prox=None, is_cap=0.0, rows=None):
+                  logp_prox=None, is_cap=0.0, rows=None, dual_clip=0.0, logp_ref=None,
+                  kl_coef=0.0, ent_coef=0.0):
     """S3 + S4 on the given logit rows. `rows` = indices into the token view (defaults to
     all); `logits` holds exactly those rows."""
     rows = np.arange(len(tv["target"])) if rows is None else np.asarray(rows)
@@ -70,16 +71,23 @@ def loss_and_grad(logits, tv, *, eps_low=0.2, eps_high=0.2, max_staleness=1, n_t
     valid = tv["valid"][rows]
     base = valid & (f["status"] == 0)
     lpp = None if logp_prox is None else np.asarray(logp_prox)[rows]
+    lpr = None if logp_ref is None else np.asarray(logp_ref)[rows]
     p = ppo_mod.ppo_loss(f["logp"], tv["logp_behav"][rows], tv["adv"][rows], base,
                          tv["lag"][rows], eps_low=eps_low, eps_high=eps_high,
                          max_staleness=max_staleness, n_tok=n_tok, logp_prox=lpp,
-                         is_cap=is_cap)
+                         is_cap=is_cap, dual_clip=dual_clip, logp_ref=lpr, kl_coef=kl_coef)
     dx = lp_mod.log_softmax_grad(logits, tgt, f["lse"], p["grad"])
+    N = p["stats"]["denom"]
+    if ent_coef:
+        coef = np.where(p["mask"], ent_coef / N if N > 0 else 0.0, 0.0)
+        dx = dx + lp_mod.entropy_bonus_grad(logits, f["lse"], f["entropy"], coef)
     bad = valid & ((f["status"] == 2) | (f["status"] == 3))
     n_bad_tok = float(bad.sum() + p["bad_lag"].sum())
     ent = float(np.where(p["mask"], f["entropy"], 0.0).sum())
     stats = dict(p["stats"])
     stats.update(entropy_sum=ent, n_bad_tok=n_bad_tok)
+    if ent_coef and N > 0:
+        stats["loss"] -= ent_coef * ent / N
     return dict(fwd=f, ppo=p, dx=dx, stats=stats)
 
 

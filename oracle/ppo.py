@@ -26,14 +26,20 @@ NEAR_TIE_REL = 1e-5
 
 
 def ppo_loss(logp, logp_behav, adv_tok, mask_base, lag_tok, *, eps_low=0.2, eps_high=0.2,
-             max_staleness=1, n_tok=None, logp_prox=None, is_cap=0.0):
+             max_staleness=1, n_tok=None, logp_prox=None, is_cap=0.0, dual_clip=0.0,
+             logp_ref=None, kl_coef=0.0):
     """Per-token PPO/decoupled loss in float64.
 
-    logp, logp_behav, logp_prox, adv_tok: [R]; mask_base: bool [R] = valid step and
-    usable target (finite logp); lag_tok: int [R].
-    Returns dict(loss_tok, grad, mask, stale, bad_lag, clipped, near_tie, ratio, w,
-    stats) where loss_tok is the unnormalised L_r (0 where masked) and grad is
-    dLoss/dlogp including the 1/N_tok factor.
+    logp, logp_behav, logp_prox, logp_ref, adv_tok: [R]; mask_base: bool [R] = valid step
+    and usable target (finite logp); lag_tok: int [R].
+    Optional terms (NEXT-2; the paper is silent, readings R19-R20):
+      dual_clip c > 1 (Ye et al. 2020): for A < 0 the objective is max(J, c A), so tokens
+        with c A > J carry no gradient ("dual-clipped");
+      kl_coef b with logp_ref (k3 estimator, Schulman 2020; as in GRPO): L += b k3,
+        k3 = e^{lr} - lr - 1, lr = logp_ref - logp, dk3/dlogp = 1 - e^{lr}.
+    Returns dict(loss_tok, grad, mask, stale, bad_lag, clipped, dual, near_tie, ratio, w,
+    stats): loss_tok is the unnormalised per-token loss (0 where masked), grad is dLoss/dlogp
+    including the 1/N_tok factor.
     """
     logp = np.asarray(logp, np.float64)
     lb = np.asarray(logp_behav, np.float64)
@@ -45,6 +51,7 @@ def ppo_loss(logp, logp_behav, adv_tok, mask_base, lag_tok, *, eps_low=0.2, eps_
     m = base & (lag >= 0) & (lag <= max_staleness)
     if n_tok is None:
         n_tok = float(m.sum())
+    inv_n = 1.0 / n_tok if n_tok > 0 else 0.0
     with np.errstate(over="ignore", invalid="ignore"):
         if logp_prox is None:
             w = np.ones_like(logp)
@@ -59,19 +66,97 @@ def ppo_loss(logp, logp_behav, adv_tok, mask_base, lag_tok, *, eps_low=0.2, eps_
         lo, hi = 1.0 - eps_low, 1.0 + eps_high
         surr1 = rho * A
         surr2 = np.clip(rho, lo, hi) * A
-        L = -w * np.minimum(surr1, surr2)
+        J = np.minimum(surr1, surr2)
         clipped = ((A > 0) & (rho > hi)) | ((A < 0) & (rho < lo))
-        grad = np.where(clipped, 0.0, -w * A * rho) / n_tok
+        dual = np.zeros_like(clipped)
+        if dual_clip and dual_clip > 1.0:
+            dual = (A < 0) & (dual_clip * A > J)
+            J = np.where(dual, dual_clip * A, J)
+        L = -w * J
+        gpg = np.where(clipped | dual, 0.0, -w * A * rho)
         near_tie = (np.abs(rho / hi - 1.0) <= NEAR_TIE_REL) | (np.abs(rho / lo - 1.0) <= NEAR_TIE_REL)
-    L = np.where(m, L, 0.0)
-    grad = np.where(m, grad, 0.0)
+        if dual_clip and dual_clip > 1.0:
+            near_tie = near_tie | (np.abs(rho / dual_clip - 1.0) <= NEAR_TIE_REL)
+        k3ref = np.zeros_like(logp)
+        gkl = np.zeros_like(logp)
+        if logp_ref is not None and kl_coef:
+            lref = np.asarray(logp_ref, np.float64) - logp
+            k3ref = np.exp(lref) - lref - 1.0
+            gkl = kl_coef * (1.0 - np.exp(lref))
+    Lpg = np.where(m, L, 0.0)
+    Ltot = np.where(m, L + kl_coef * k3ref, 0.0)
+    grad = np.where(m, (gpg + gkl) * inv_n, 0.0)
     clipped = clipped & m
+    dual = dual & m
     k3 = np.where(m, rho - 1.0 - lr, 0.0)
-    stats = dict(loss=L.sum() / n_tok if n_tok > 0 else 0.0,
-                 n_clipped=float(clipped.sum()), kl_k3_sum=float(k3.sum()),
+    stats = dict(loss=Ltot.sum() * inv_n, pg_loss=Lpg.sum() * inv_n,
+                 n_clipped=float(clipped.sum()), n_dual_clipped=float(dual.sum()),
+                 kl_k3_sum=float(k3.sum()), kl_ref_sum=float(np.where(m, k3ref, 0.0).sum()),
                  ratio_sum=float(np.where(m, rho, 0.0).sum()),
                  n_loss_tok=float(m.sum()), n_stale_tok=float(stale.sum()),
                  n_bad_lag=float(bad_lag.sum()),
                  logp_sum=float(np.where(m, logp, 0.0).sum()), denom=float(n_tok))
-    return dict(loss_tok=L, grad=grad, mask=m, stale=stale, bad_lag=bad_lag, clipped=clipped,
-                near_tie=near_tie & m, ratio=rho, w=w, stats=stats)
+    return dict(loss_tok=Ltot, grad=grad, mask=m, stale=stale, bad_lag=bad_lag, clipped=clipped,
+                dual=dual, near_tie=near_tie & m, ratio=rho, w=w, stats=stats)
+
+
+def ppo_loss_chunk(logp, logp_behav, adv_step, mask_tok, step_of_tok, n_steps_total, *,
+                   eps_low=0.2, eps_high=0.2, n_den=None):
+    """Chunk-level ratio (NEXT-2, reading R21): one ratio per decision step = the action
+    chunk's likelihood ratio rho_s = exp(sum_{a in s, m_a} (logp_a - logp_behav_a)) (an
+    OpenVLA-OFT action chunk is one inference); L_s = -min(rho_s A_s, clip(rho_s) A_s)
+    over steps with >= 1 masked token; Loss = sum_s L_s / N_steps; every token of step s gets
+    dLoss/dlogp = -A_s rho_s [active_s] / N_steps."""
+    logp = np.asarray(logp, np.float64)
+    lb = np.asarray(logp_behav, np.float64)
+    m = np.asarray(mask_tok, bool)
+    st = np.asarray(step_of_tok, np.int64)
+    A = np.asarray(adv_step, np.float64)
+    lr = np.zeros(n_steps_total)
+    cnt = np.zeros(n_steps_total)
+    for r in range(len(logp)):
+        if m[r]:
+            lr[st[r]] += logp[r] - lb[r]
+            cnt[st[r]] += 1
+    ms = cnt > 0
+    N = float(ms.sum()) if n_den is None else n_den
+    inv = 1.0 / N if N > 0 else 0.0
+    rho = np.exp(lr)
+    lo, hi = 1.0 - eps_low, 1.0 + eps_high
+    J = np.minimum(rho * A, np.clip(rho, lo, hi) * A)
+    clipped = ((A > 0) & (rho > hi)) | ((A < 0) & (rho < lo))
+    g_step = np.where(ms & ~clipped, -A * rho * inv, 0.0)
+    grad = np.where(m, g_step[st], 0.0)
+    L = np.where(ms, -J, 0.0)
+    return dict(grad=grad, loss_step=L, rho_step=rho, mask_step=ms, clipped=clipped & ms,
+                stats=dict(loss=L.sum() * inv, n_clipped=float((clipped & ms).sum()),
+                           n_steps=float(ms.sum()), denom=N))
+
+
+def value_loss(v_new, v_old, ret, mask, *, clip_eps=0.2, n_den=None):
+    """Clipped value loss per decision step (PPO value head, NEXT-2; paper-silent, reading
+    R22): L = 0.5 max((v - R)^2, (v_old + clip(v - v_old, -e, e) - R)^2); e <= 0 => plain
+    0.5 (v - R)^2. Loss = sum m L / N; dLoss/dv from the larger branch (ties: unclipped),
+    the clipped branch passing gradient only inside the clip interval."""
+    v = np.asarray(v_new, np.float64)
+    vo = np.asarray(v_old, np.float64)
+    R = np.asarray(ret, np.float64)
+    m = np.asarray(mask, bool)
+    N = float(m.sum()) if n_den is None else n_den
+    inv = 1.0 / N if N > 0 else 0.0
+    u = (v - R) ** 2
+    if clip_eps and clip_eps > 0:
+        d = v - vo
+        vc = vo + np.clip(d, -clip_eps, clip_eps)
+        c = (vc - R) ** 2
+        use_c = c > u
+        g = np.where(use_c, (vc - R) * (np.abs(d) < clip_eps), v - R)
+        L = 0.5 * np.maximum(u, c)
+    else:
+        use_c = np.zeros_like(m)
+        g = v - R
+        L = 0.5 * u
+    return dict(loss_step=np.where(m, L, 0.0), grad=np.where(m, g * inv, 0.0),
+                clipped=use_c & m,
+                stats=dict(loss=np.where(m, L, 0.0).sum() * inv, n_clipped=float((use_c & m).sum()),
+                           n_steps=float(m.sum()), denom=N))

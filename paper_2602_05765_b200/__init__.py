@@ -7,6 +7,6 @@ load the library; the first call does, and raises if librlvla.so has not been bu
 from .api import (  # noqa: F401
     Comm, RlvlaError, StepBatch, TrajectoryBuffer, adv_params, logits_desc, ppo_args,
     rlvla_abi_version, rlvla_advantages, rlvla_logprob_fwd_bwd, rlvla_nccl_version,
-    rlvla_ppo_loss, rlvla_scatter_steps, rlvla_workspace_bytes, workspace)
+    rlvla_ppo_loss, rlvla_scatter_steps, rlvla_value_loss, rlvla_workspace_bytes, workspace)
 from . import _abi as abi  # noqa: F401
 from . import sharding  # noqa: F401

@@ -16,11 +16,12 @@ HEADER = os.path.join(ROOT, "include", "rlvla.h")
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_NCCL, ERR_DATA = range(6)
 F32, BF16 = 0, 1
 ADV_GAE, ADV_GRPO = 0, 1
-NSTATS = 16
+NSTATS = 24
 (STAT_N_VALID_STEPS, STAT_SUM_ADV, STAT_SUM_ADV2, STAT_N_TOK, STAT_N_STALE_STEPS,
  STAT_N_BAD_STEPS, STAT_LOSS, STAT_N_CLIPPED, STAT_KL_K3_SUM, STAT_ENTROPY_SUM,
  STAT_RATIO_SUM, STAT_N_LOSS_TOK, STAT_N_STALE_TOK, STAT_N_BAD_TOK, STAT_LOGP_SUM,
- STAT_DENOM) = range(16)
+ STAT_KL_REF_SUM, STAT_N_DUAL_CLIPPED, STAT_PG_LOSS, STAT_DENOM, STAT_VALUE_LOSS,
+ STAT_N_VALUE_CLIPPED, STAT_N_VALUE_STEPS, STAT_VALUE_DENOM, STAT_RESERVED) = range(24)
 CNT_OOB, CNT_BAD_VERSION, CNT_DUP, CNT_WRITTEN = range(4)
 
 
@@ -41,7 +42,8 @@ class c_adv_params(ctypes.Structure):
     _fields_ = [("mode", c_int32), ("gamma", c_float), ("lam", c_float), ("whiten", c_int32),
                 ("whiten_eps", c_float), ("group_id", c_void_p), ("group_size", c_int32),
                 ("std_unbiased", c_int32), ("grpo_eps", c_float), ("env_offset", c_int32),
-                ("n_env_global", c_int32), ("cur_version", c_int32), ("max_staleness", c_int32)]
+                ("n_env_global", c_int32), ("cur_version", c_int32), ("max_staleness", c_int32),
+                ("boot_value", c_void_p)]
 
 
 class c_logits(ctypes.Structure):
@@ -55,7 +57,9 @@ class c_ppo_args(ctypes.Structure):
                 ("cur_version", c_int32), ("max_staleness", c_int32), ("eps_low", c_float),
                 ("eps_high", c_float), ("is_cap", c_float), ("tok_denominator", c_double),
                 ("adv_stats", c_void_p), ("out_grad_logp", c_void_p),
-                ("out_loss_tok", c_void_p), ("accumulate", c_int32)]
+                ("out_loss_tok", c_void_p), ("accumulate", c_int32), ("dual_clip", c_float),
+                ("logp_ref", c_void_p), ("kl_coef", c_float), ("ent_coef", c_float),
+                ("ratio_level", c_int32)]
 
 
 _SIGS = {
@@ -69,6 +73,9 @@ _SIGS = {
                                         c_void_p, c_size_t, c_void_p, c_void_p]),
     "rlvla_ppo_loss": (c_int32, [c_void_p, c_int64, c_void_p, POINTER(c_ppo_args), c_void_p,
                                  c_void_p, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
+    "rlvla_value_loss": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
+                                   c_int32, c_int32, c_float, c_double, c_void_p, c_void_p,
+                                   c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
     "rlvla_workspace_bytes": (c_size_t, [c_int64, c_int32, c_int32]),
     "rlvla_comm_unique_id": (c_int32, [c_void_p]),
     "rlvla_comm_init": (c_int32, [c_void_p, c_int32, c_int32, POINTER(c_void_p)]),

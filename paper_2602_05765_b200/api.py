@@ -135,11 +135,11 @@ def rlvla_scatter_steps(buf: TrajectoryBuffer, rec: StepBatch, cur_version: int,
 
 def adv_params(mode, *, gamma=0.99, lam=0.95, whiten=False, whiten_eps=1e-8, group_id=None,
                group_size=0, std_unbiased=True, grpo_eps=1e-6, env_offset=0, n_env_global=0,
-               cur_version=0, max_staleness=1) -> A.c_adv_params:
+               cur_version=0, max_staleness=1, boot_value=None) -> A.c_adv_params:
     p = A.c_adv_params(A.ADV_GAE if mode == "gae" else A.ADV_GRPO, gamma, lam, int(whiten),
                        whiten_eps, _ptr(group_id), group_size, int(std_unbiased), grpo_eps,
-                       env_offset, n_env_global, cur_version, max_staleness)
-    p._keep = (group_id,)      # the struct holds raw pointers: keep the tensors alive
+                       env_offset, n_env_global, cur_version, max_staleness, _ptr(boot_value))
+    p._keep = (group_id, boot_value)  # the struct holds raw pointers: keep the tensors alive
     return p
 
 
@@ -163,14 +163,16 @@ def logits_desc(x: torch.Tensor, vocab: int | None = None) -> A.c_logits:
 def ppo_args(*, logp_behav, adv, version, slot_key, a_tok, cur_version, max_staleness=1,
              eps_low=0.2, eps_high=0.2, is_cap=0.0, logp_prox=None, tok_denominator=0.0,
              adv_stats=None, out_grad_logp=None, out_loss_tok=None,
-             accumulate=False) -> A.c_ppo_args:
+             accumulate=False, dual_clip=0.0, logp_ref=None, kl_coef=0.0, ent_coef=0.0,
+             ratio_level=0) -> A.c_ppo_args:
     a = A.c_ppo_args(_ptr(logp_behav), _ptr(logp_prox), _ptr(adv), _ptr(version),
                      _ptr(slot_key), a_tok, cur_version, max_staleness, eps_low, eps_high,
                      is_cap, tok_denominator, _ptr(adv_stats), _ptr(out_grad_logp),
-                     _ptr(out_loss_tok), int(accumulate))
+                     _ptr(out_loss_tok), int(accumulate), dual_clip, _ptr(logp_ref), kl_coef,
+                     ent_coef, ratio_level)
     # the struct holds raw pointers: keep the tensors alive as long as the struct
     a._keep = (logp_behav, logp_prox, adv, version, slot_key, adv_stats, out_grad_logp,
-               out_loss_tok)
+               out_loss_tok, logp_ref)
     return a
 
 
@@ -194,6 +196,18 @@ def rlvla_ppo_loss(logp, target, args: A.c_ppo_args, grad_logp, loss_tok=None, s
                               _ptr(grad_logp), _ptr(loss_tok), _ptr(stats), wp, wn,
                               comm.handle if comm is not None else None, _stream(stream))
     return _check(st, "rlvla_ppo_loss", check)
+
+
+def rlvla_value_loss(v_new, v_old, ret, slot_key, version, cur_version, grad_v, *,
+                     max_staleness=1, clip_eps=0.2, denominator=0.0, loss_step=None,
+                     stats=None, ws=None, comm=None, stream=None, check=True) -> int:
+    wp, wn = _ws_ptr(ws)
+    st = lib().rlvla_value_loss(_ptr(v_new), _ptr(v_old), _ptr(ret), _ptr(slot_key),
+                                _ptr(version), v_new.numel(), cur_version, max_staleness,
+                                clip_eps, denominator, _ptr(grad_v), _ptr(loss_step),
+                                _ptr(stats), wp, wn,
+                                comm.handle if comm is not None else None, _stream(stream))
+    return _check(st, "rlvla_value_loss", check)
 
 
 def rlvla_workspace_bytes(rows: int, n_env_global: int, t_steps: int) -> int:

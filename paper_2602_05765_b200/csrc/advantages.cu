@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) gae_scan_kernel(AdvArgs a) {
       const int t = tile * 32 + lane;
       const bool in = t < T;
       const int64_t idx = int64_t(e) * T + t;
-      float r = 0.f, V = 0.f;
+      float r = 0.f, V = 0.f, B = 0.f;
       int d = 0, v = 0, ver = 0;
       if (in) {
         r = a.buf.reward[idx];
@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(256) gae_scan_kernel(AdvArgs a) {
         d = a.buf.done[idx];
         v = a.buf.slot_key[idx] != 0ull;
         ver = a.buf.version[idx];
+        if (d == 2 && a.p.boot_value) B = a.p.boot_value[idx];  // truncation bootstrap
       }
       float Vn = __shfl_down_sync(0xffffffffu, V, 1);
       int vn = __shfl_down_sync(0xffffffffu, v, 1);
@@ -84,8 +85,10 @@ __global__ void __launch_bounds__(256) gae_scan_kernel(AdvArgs a) {
         Vn = lv;
         vn = 1;
       }
-      const float nt = (v && !d && vn) ? 1.f : 0.f;
-      float D = v ? (r + gamma * nt * Vn - V) : 0.f;
+      // done 1 = termination, 2 = time-limit truncation (recursion cut, bootstrap from B)
+      const float nt = (v && d == 0 && vn) ? 1.f : 0.f;
+      const float tr = (d == 2) ? 1.f : 0.f;
+      float D = v ? (r + gamma * fmaf(nt, Vn, tr * B) - V) : 0.f;
       float C = gl * nt;
       if (!in) {  // identity map on padding lanes
         D = 0.f;

@@ -84,9 +84,13 @@ rlvla_status check_ppo_args(const rlvla_ppo_args* f) {
   if (!f->logp_behav || !f->adv || !f->version || !f->slot_key) return RLVLA_ERR_INVALID_ARG;
   if (f->a_tok <= 0 || f->max_staleness < 0) return RLVLA_ERR_INVALID_ARG;
   if (!(f->eps_low >= 0.f) || !(f->eps_high >= 0.f) || f->eps_low >= 1.f) return RLVLA_ERR_INVALID_ARG;
-  if (!(f->tok_denominator > 0.0) && !f->adv_stats) return RLVLA_ERR_INVALID_ARG;
+  if (!(f->tok_denominator > 0.0) && !f->adv_stats && f->ratio_level == 0) return RLVLA_ERR_INVALID_ARG;
   if (reinterpret_cast<uintptr_t>(f->slot_key) % 8) return RLVLA_ERR_INVALID_ARG;
   if (f->accumulate != 0 && f->accumulate != 1) return RLVLA_ERR_INVALID_ARG;
+  if (f->ratio_level != 0 && f->ratio_level != 1) return RLVLA_ERR_INVALID_ARG;
+  if (!(f->dual_clip <= 0.f || f->dual_clip > 1.f)) return RLVLA_ERR_INVALID_ARG;
+  if (f->kl_coef != 0.f && !f->logp_ref) return RLVLA_ERR_INVALID_ARG;
+  if (!(f->ent_coef == f->ent_coef) || !(f->kl_coef == f->kl_coef)) return RLVLA_ERR_INVALID_ARG;
   return RLVLA_OK;
 }
 
@@ -220,6 +224,7 @@ RLVLA_API rlvla_status rlvla_logprob_fwd_bwd(const rlvla_logits* x, const int32_
     rlvla_status st = check_ppo_args(fused);
     if (st != RLVLA_OK) return st;
     if (x->rows % fused->a_tok) return RLVLA_ERR_INVALID_ARG;
+    if (fused->ratio_level != 0) return RLVLA_ERR_UNSUPPORTED;  // chunk ratio: rlvla_ppo_loss
   }
   if (stats && !grad_logp) {
     if (!workspace || ws_bytes < ws_bytes_for(1) || reinterpret_cast<uintptr_t>(workspace) % kAlignWs)
@@ -257,8 +262,9 @@ RLVLA_API rlvla_status rlvla_ppo_loss(const float* logp, int64_t rows, const int
   rlvla_status st = check_ppo_args(f);
   if (st != RLVLA_OK) return st;
   if (rows % f->a_tok) return RLVLA_ERR_INVALID_ARG;
-  if (stats && (!workspace || ws_bytes < ws_bytes_for(1) ||
-                reinterpret_cast<uintptr_t>(workspace) % kAlignWs))
+  if (f->ent_coef != 0.f) return RLVLA_ERR_UNSUPPORTED;  // the entropy bonus needs the logits
+  if ((stats || f->ratio_level == 1) &&
+      (!workspace || ws_bytes < ws_bytes_for(1) || reinterpret_cast<uintptr_t>(workspace) % kAlignWs))
     return RLVLA_ERR_INVALID_ARG;
   if (rows == 0) return RLVLA_OK;
   if (!device_ready()) return RLVLA_ERR_CUDA;
@@ -280,6 +286,32 @@ RLVLA_API rlvla_status rlvla_ppo_loss(const float* logp, int64_t rows, const int
     return sync_check_stats(stats, RLVLA_STAT_N_BAD_TOK, s);
   }
   return RLVLA_OK;
+}
+
+RLVLA_API rlvla_status rlvla_value_loss(const float* v_new, const float* v_old, const float* ret,
+                                        const uint64_t* slot_key, const int32_t* version,
+                                        int64_t n_steps, int32_t cur_version,
+                                        int32_t max_staleness, float clip_eps,
+                                        double denominator, float* grad_v, float* loss_step,
+                                        double* stats, void* workspace, size_t ws_bytes,
+                                        rlvla_comm comm, void* stream) {
+  if (!v_new || !ret || !slot_key || !version || !grad_v || n_steps < 0 || max_staleness < 0)
+    return RLVLA_ERR_INVALID_ARG;
+  if (clip_eps > 0.f && !v_old) return RLVLA_ERR_INVALID_ARG;
+  if (!(clip_eps == clip_eps)) return RLVLA_ERR_INVALID_ARG;
+  if (!workspace || ws_bytes < ws_bytes_for(1) || reinterpret_cast<uintptr_t>(workspace) % kAlignWs)
+    return RLVLA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(slot_key) % 8 || (stats && reinterpret_cast<uintptr_t>(stats) % 8))
+    return RLVLA_ERR_INVALID_ARG;
+  if (n_steps == 0) return RLVLA_OK;
+  if (!device_ready()) return RLVLA_ERR_CUDA;
+  ValueArgs a{v_new, v_old, ret, slot_key, version, n_steps, cur_version, max_staleness, clip_eps,
+              denominator, grad_v, loss_step, stats, carve(workspace)};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  rlvla_status st = cuda_status(launch_value_loss(a, s));
+  if (st != RLVLA_OK || !stats) return st;
+  return allreduce_stats(stats + RLVLA_STAT_VALUE_LOSS,
+                         RLVLA_STAT_VALUE_DENOM - RLVLA_STAT_VALUE_LOSS, comm, s);
 }
 
 RLVLA_API rlvla_status rlvla_comm_unique_id(void* out) {

@@ -17,7 +17,8 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
 // control-word indices (uint32 each) inside the workspace header
-enum { CTRL_SCATTER = 0, CTRL_ADV = 1, CTRL_LOGPROB = 2, CTRL_PPO = 3, CTRL_ADV2 = 4 };
+enum { CTRL_SCATTER = 0, CTRL_ADV = 1, CTRL_LOGPROB = 2, CTRL_PPO = 3, CTRL_ADV2 = 4, CTRL_VALUE = 5 };
+// ctrl words 32..35 hold two doubles of per-call scratch (chunk-ratio and value-loss 1/N)
 
 struct Workspace {
   unsigned* ctrl;      // [64]
@@ -252,5 +253,22 @@ struct PpoArgs {
   Workspace ws;
 };
 cudaError_t launch_ppo_loss(const PpoArgs& a, cudaStream_t s);
+
+struct ValueArgs {
+  const float* v_new;
+  const float* v_old;
+  const float* ret;
+  const uint64_t* slot_key;
+  const int32_t* version;
+  int64_t n;
+  int32_t cur_version, max_staleness;
+  float clip_eps;
+  double denominator;
+  float* grad_v;
+  float* loss_step;
+  double* stats;
+  Workspace ws;
+};
+cudaError_t launch_value_loss(const ValueArgs& a, cudaStream_t s);
 
 }  // namespace rlvla

@@ -4,18 +4,12 @@
 //
 // Definition (P:39 action tokens; textbook log-softmax, reading R3-R5):
 //   lse = m + ln sum_j e^{x_j - m}, logp = x_a - lse, H = lse - sum_j p_j x_j,
-//   dx_j = g (1[j=a] - p_j).
+//   dx_j = g (1[j=a] - p_j) [+ c p_j (log p_j + H) with the entropy bonus, c = m beta_H/N].
 //
 // Three kernels, one per size class:
-//   lp_tma_kernel     bf16, 2048 < V <= 32768 (OpenVLA 32000 vocab). Persistent, one
-//                     1024-thread CTA per SM. Rows are staged HBM -> SMEM by the TMA engine
-//                     (cp.async.bulk, 1-D, 64 KB per row, up to 4-stage ring, mbarrier
-//                     completion, L2 evict_first). Each thread owns 4 x 16 B of the row,
-//                     keeps e_j = 2^{(x_j - m_warp) log2e} in registers (ONE ex2 per
-//                     element), one __syncthreads per row combines the 32 warp partials,
-//                     and dlogits leave as 128-bit streaming stores straight from
-//                     registers. The refill of the freed stage is issued right after
-//                     the barrier, so 2-3 rows are in flight per SM.
+//   lp_tma_kernel     bf16, 2048 < V <= 32768 (OpenVLA 32000 vocab). Persistent, one CTA
+//                     per SM, two independent 512-thread row groups; rows staged HBM ->
+//                     SMEM by TMA bulk copies in a 3-stage ring (details at the kernel).
 //   lp_warp_kernel    V <= 2048 (e.g. the 256-bin tiny config): one warp per row,
 //                     register-resident row via 128-bit loads.
 //   lp_generic_kernel any V / alignment / dtype: one CTA per row, three passes.
@@ -33,6 +27,11 @@ enum { MODE_FWD = 0, MODE_FUSED = 1, MODE_BWD = 2 };
 // (Measured and rejected: a NaN-guarded per-vector redo instead of the per-element -inf
 // clamp in the entropy partial — 4% slower, the per-vector branch costs more than it saves.)
 
+constexpr uint32_t kNegClampPair = 0xF180F180u;  // bf16x2 (-2^100, -2^100)
+
+// -inf -> -1e30, NaN kept (a comparison with NaN is false)
+__device__ __forceinline__ float clamp_ninf(float t) { return t < -1e30f ? -1e30f : t; }
+
 struct Lp {
   const void* x;
   int64_t rows;
@@ -47,6 +46,7 @@ struct Lp {
   // fused PPO
   const float* lpb;
   const float* lpp;
+  const float* lref;
   const float* adv;
   const int32_t* ver;
   const uint64_t* key;
@@ -84,27 +84,41 @@ __device__ __forceinline__ int row_status(int a, int V, float lse, float logp) {
   return 0;
 }
 
-// Per-row outputs shared by all kernels once (lse, logp, H) are known. Every caller
-// thread gets g; `writer` threads store the per-row outputs and accumulate stats.
+struct RowMeta {
+  float lpb = 0.f, lpp = 0.f, lref = 0.f, adv = 0.f;
+  int ver = 0;
+  uint64_t key = 1;
+};
+
+// The row's PPO quantities once (lse, logp, H) are known: g = dLoss/dlogp and the entropy
+// bonus weight c = ent_coef * m / N.
+struct RowGrad {
+  float g;
+  float c;
+};
+
+// `writer` stores the per-row outputs and accumulates the statistics
 template <int MODE>
-__device__ __forceinline__ float finish_row(const Lp& p, const PpoConst& pc, int64_t r, int a,
-                                            float lse, float logp,
-                                            float H, float lpb, float lpp, float advv, int ver,
-                                            uint64_t key, bool writer, double* acc) {
+__device__ __forceinline__ RowGrad finish_row(const Lp& p, const PpoConst& pc, int64_t r, int a,
+                                              float lse, float logp, float H, const RowMeta& mt,
+                                              bool writer, double* acc) {
   const int st = row_status(a, p.V, lse, logp);
-  float g = 0.f, lt = 0.f;
+  RowGrad out{0.f, 0.f};
+  float lt = 0.f;
   RowStats rs;
   PpoRowIn in;
   in.tgt_status = st;
   in.logp = (st == 1 || st == 2) ? 0.f : logp;
   in.H = H;
   if (MODE == MODE_FUSED) {
-    in.lpb = lpb;
-    in.lpp = lpp;
-    in.adv = advv;
-    in.ver = ver;
-    in.valid = key != 0ull;
-    g = ppo_row(pc, in, rs, &lt);
+    in.lpb = mt.lpb;
+    in.lpp = mt.lpp;
+    in.lref = mt.lref;
+    in.adv = mt.adv;
+    in.ver = mt.ver;
+    in.valid = mt.key != 0ull;
+    out.g = ppo_row(pc, in, rs, &lt);
+    out.c = rs.m != 0.f ? pc.ent_coef * pc.invN : 0.f;
   } else {
     fwd_row_stats(in, rs);
   }
@@ -112,12 +126,27 @@ __device__ __forceinline__ float finish_row(const Lp& p, const PpoConst& pc, int
     p.logp[r] = in.logp;
     if (p.lse_out) p.lse_out[r] = lse;
     if (MODE == MODE_FUSED) {
-      if (p.out_g) p.out_g[r] = g;
+      if (p.out_g) p.out_g[r] = out.g;
       if (p.out_L) p.out_L[r] = lt;
     }
     if (acc) acc_stats(acc, rs);
   }
-  return g;
+  return out;
+}
+
+template <int MODE>
+__device__ __forceinline__ RowMeta load_meta(const Lp& p, int64_t r) {
+  RowMeta m;
+  if (MODE == MODE_FUSED) {
+    const int64_t s = r / p.A;
+    m.lpb = p.lpb[r];
+    if (p.lpp) m.lpp = p.lpp[r];
+    if (p.lref) m.lref = p.lref[r];
+    m.adv = p.adv[s];
+    m.ver = p.ver[s];
+    m.key = p.key[s];
+  }
+  return m;
 }
 
 // N for 1/N and the per-kernel copy of the PPO constants
@@ -126,6 +155,7 @@ __device__ __forceinline__ double resolve_pc(const Lp& p, PpoConst& pc) {
   pc = p.pc;
   if (MODE != MODE_FUSED) {
     pc.invN = 0.f;
+    pc.ent_coef = 0.f;
     return 0.0;
   }
   const double N = loss_denominator(p.N, p.adv_stats);
@@ -133,21 +163,29 @@ __device__ __forceinline__ double resolve_pc(const Lp& p, PpoConst& pc) {
   return N;
 }
 
+// dx at the target column: g (1 - p_a) + c p_a (log p_a + H), with 1 - p_a = S_rest / S
+__device__ __forceinline__ float target_grad(const RowGrad& rg, float Srest, float ea, float invS,
+                                             float logp, float H) {
+  return rg.g * Srest * invS + (rg.c != 0.f ? rg.c * ea * invS * (logp + H) : 0.f);
+}
+
 // =====================================================================================
 // K6/K5/K7 for bf16 rows up to 32768: TMA-staged persistent kernel, two row groups
 // =====================================================================================
 // One 1024-thread CTA per SM, split into two independent 512-thread groups; group g
 // processes the CTA's rows k = g, g+2, ... Rows live in a ring of nst SMEM stages filled
-// by the TMA engine (1-D bulk copies, mbarrier tx-count completion); row k uses stage
-// k % nst. Per row a group makes three passes over the SMEM copy:
+// by the TMA engine (1-D bulk copies, mbarrier tx-count completion, L2 evict_first); row k
+// uses stage k % nst. Per row a group makes three passes over the SMEM copy:
 //   A  max over its 16-byte vectors (packed bf16x2 max, no MUFU)
-//   B  e = 2^{(x - m_warp) log2e} (one ex2), sum and entropy partials per warp
-//   -- named barrier; warp 0 combines the 16 warp partials, runs the per-row epilogue
-//      (lse, logp, H, PPO g, stats) and publishes the row scalars; named barrier --
-//   C  dx = -g/S * 2^{(x - M) log2e} (second ex2), packed to bf16, 128-bit stores
-// then releases the stage by issuing the TMA for row k + nst into it. While one group
-// sits in its latency-bound combine/epilogue the other streams, so the SM never idles
-// at a CTA-wide barrier; nothing row-sized is kept in registers (no spills).
+//   B  e = 2^{(x - m_warp) log2e} (one ex2), sum and entropy partials per warp; with
+//      dlogits requested (and no entropy bonus) e is written back into the stage as bf16
+//   -- named barrier #1; warp 0 combines the 16 warp partials, runs the per-row epilogue
+//      (lse, logp, H, PPO g) and publishes the row scalars with bar.arrive (#2) before
+//      finishing the per-row outputs and statistics --
+//   C  dlogits: from the stored e, dx = g' 2^{(m_w - M) log2e} e (no second ex2); or,
+//      with the entropy bonus / in external-bwd mode, from x: dx = 2^t (k1 + k2 t)
+// then (#3) releases the stage by issuing the TMA for row k + nst into it. While one
+// group sits in its latency-bound combine/epilogue the other streams.
 constexpr int kCtaThreads = 1024;
 constexpr int kGroupThreads = 512;
 constexpr int kGroupWarps = kGroupThreads / 32;
@@ -161,18 +199,22 @@ struct __align__(16) StageMeta {
   float lse_in, g_in;
   int32_t issued_row;  // row whose load was issued into this stage (plain st.shared)
   uint64_t key;
-  uint64_t pad2;
+  float lref;
+  float pad;
 };
 
 __device__ __forceinline__ int ld_volatile_s32(const int32_t* p) {
   return *reinterpret_cast<const volatile int32_t*>(p);
 }
 
+// per-row scalars published by warp 0 for pass C
 struct __align__(16) RowScalars {
-  float mL;      // M * log2e (pass C exponent offset)
-  float kscale;  // -g / S_tot
-  float ga;      // dx at the target column: g * S_rest / S_tot
-  float g;
+  float M;       // row max (pass C: per-warp scale 2^{(m_w - M) log2e}; x-path offset)
+  float k1;      // keep-e path: -g / S; x path: (-g + c (H - ln S)) / S
+  float k2;      // x path: c ln2 / S (entropy bonus), else 0
+  float ga;      // dx at the target column
+  float active;  // 0 => the row's dlogits are exactly zero
+  float pad[3];
 };
 
 template <int MODE>
@@ -184,6 +226,7 @@ __device__ __forceinline__ void issue_row(const Lp& p, int r, uint8_t* dst, Stag
     const int s = r / p.A;
     cp_async4(&m->lpb, p.lpb + r);
     if (p.lpp) cp_async4(&m->lpp, p.lpp + r);
+    if (p.lref) cp_async4(&m->lref, p.lref + r);
     cp_async4(&m->adv, p.adv + s);
     cp_async4(&m->ver, p.ver + s);
     cp_async8(&m->key, p.key + s);
@@ -199,7 +242,6 @@ __device__ __forceinline__ void issue_row(const Lp& p, int r, uint8_t* dst, Stag
 __device__ __forceinline__ void group_sync(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(kGroupThreads) : "memory");
 }
-
 __device__ __forceinline__ void advance_stage(int& st, uint32_t& ph, int nstages) {
   st += 2;
   if (st >= nstages) {
@@ -207,7 +249,6 @@ __device__ __forceinline__ void advance_stage(int& st, uint32_t& ph, int nstages
     ph ^= 1u;
   }
 }
-
 // barrier #2 (row scalars published) uses its own id (3 + g) so that warp 0, which only
 // arrives on it, can never be counted into another phase of the #1/#3 barrier (1 + g)
 __device__ __forceinline__ void scalars_arrive(int g) {
@@ -238,13 +279,13 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
   const int rows = int(p.rows);
   const int nrow = rows > first ? (rows - first + stride - 1) / stride : 0;
   const bool want_stats = p.stats != nullptr && MODE != MODE_BWD;
-  // FUSED with dlogits: pass B keeps e = 2^{(x - m_warp) log2e} in the stage as bf16 (in
-  // place of x) and pass C only rescales it -- one ex2 per element in total
-  const bool has_c = MODE == MODE_BWD || (MODE == MODE_FUSED && p.dx != nullptr);
-  const bool keep_e = MODE == MODE_FUSED && p.dx != nullptr;
-  const float L2E = kLog2e;
   PpoConst pc;
   const double Nden = resolve_pc<MODE>(p, pc);
+  // pass C runs in external-bwd mode and in fused mode with dlogits; it reuses the e
+  // values of pass B (stored as bf16 in the stage) unless the entropy bonus needs x
+  const bool has_c = MODE == MODE_BWD || (MODE == MODE_FUSED && p.dx != nullptr);
+  const bool keep_e = MODE == MODE_FUSED && p.dx != nullptr && pc.ent_coef == 0.f;
+  const float L2E = kLog2e;
 
   if (tid == 0) {
     for (int s = 0; s < nstages; ++s) mbar_init(&full[s], 2);
@@ -285,7 +326,8 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     // warp partials double-buffered by row parity: rows k and k+2 of a group never share
     float4* gred = red + (((k >> 1) & 1) * 2 + grp) * kGroupWarps;
     float* gxa = xa_s + ((k >> 1) & 1) * 2 + grp;  // raw target logit, same double buffering
-    float g = 0.f, kscale = 0.f, ga = 0.f, mL = 0.f, mws = 0.f;
+    RowScalars rsv;
+    float mws = 0.f;
 
     if (MODE != MODE_BWD) {
       // ---- pass A: thread max -> warp max (packed bf16x2 max, exact) ----------------
@@ -316,7 +358,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
           // those columns without a per-element clamp; NaN and +inf pass through unchanged
           uint32_t c4[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) c4[q] = bmax2_nan(w4[q], 0xF180F180u);
+          for (int q = 0; q < 4; ++q) c4[q] = bmax2_nan(w4[q], kNegClampPair);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const float t0 = fmaf(bf_lo(c4[q]), L2E, nmL);
@@ -368,15 +410,14 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
       if (lane == 0) gred[gw] = make_float4(mw, s, et, 0.f);
       if (keep_e) fence_proxy_async();  // generic smem writes before the stage's next TMA fill
       // warp 0 needs the row metadata; read it before the stage can be refilled
-      float lpb = 0.f, lpp = 0.f, advv = 0.f;
-      int ver = 0;
-      uint64_t key = 1;
+      RowMeta rm;
       if (gw == 0 && MODE == MODE_FUSED) {
-        lpb = mt->lpb;
-        if (p.lpp) lpp = mt->lpp;
-        advv = mt->adv;
-        ver = mt->ver;
-        key = mt->key;
+        rm.lpb = mt->lpb;
+        if (p.lpp) rm.lpp = mt->lpp;
+        if (p.lref) rm.lref = mt->lref;
+        rm.adv = mt->adv;
+        rm.ver = mt->ver;
+        rm.key = mt->key;
       }
       group_sync(grp);  // #1: warp partials + x_a visible; stage no longer read in FWD mode
       if (!has_c && gt == 0 && k + nstages < nrow) {
@@ -401,41 +442,20 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
         const float invS = __fdividef(1.f, Stot);
         const float Ctot = Csum + (tgt_ok ? ea * fmaxf(ta, -256.f) : 0.f);
         const float H = lnS - Ctot * invS * kLn2;
-        const int stt = row_status(a, V, lse_row, logp);
-        PpoRowIn in;
-        in.tgt_status = stt;
-        in.logp = (stt == 1 || stt == 2) ? 0.f : logp;
-        in.H = H;
-        in.lpb = lpb;
-        in.lpp = lpp;
-        in.adv = advv;
-        in.ver = ver;
-        in.valid = key != 0ull;
-        RowStats rs;
-        float lt = 0.f;
-        if (MODE == MODE_FUSED) g = ppo_row(pc, in, rs, &lt);
-        else fwd_row_stats(in, rs);
+        const RowGrad rg = finish_row<MODE>(p, pc, r, a, lse_row, logp, H, rm, lane == 0,
+                                            want_stats ? gacc + grp * 16 : nullptr);
         if (has_c) {
           if (lane == 0) {
             RowScalars sc4;
-            sc4.mL = M;                    // pass C: per-warp scale 2^{(m_w - M) log2e}
-            sc4.kscale = -g * invS;
-            sc4.ga = g * Srest * invS;
-            sc4.g = g;
+            sc4.M = (M == -INFINITY) ? 0.f : M;
+            sc4.k1 = keep_e ? -rg.g * invS : (-rg.g + rg.c * (H - lnS)) * invS;
+            sc4.k2 = keep_e ? 0.f : rg.c * kLn2 * invS;
+            sc4.ga = target_grad(rg, Srest, ea, invS, logp, H);
+            sc4.active = (rg.g != 0.f || rg.c != 0.f) ? 1.f : 0.f;
             rsc[grp] = sc4;
           }
           __syncwarp();
           scalars_arrive(grp);  // #2 (producer side): the other warps may start pass C now
-        }
-        // per-row outputs and statistics, off the pass-C critical path
-        if (lane == 0) {
-          p.logp[r] = in.logp;
-          if (p.lse_out) p.lse_out[r] = lse_row;
-          if (MODE == MODE_FUSED) {
-            if (p.out_g) p.out_g[r] = g;
-            if (p.out_L) p.out_L[r] = lt;
-          }
-          if (want_stats) acc_stats(gacc + grp * 16, rs);
         }
       } else if (has_c) {
         scalars_sync(grp);  // #2 (consumer side): row scalars published
@@ -444,56 +464,49 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
         advance_stage(st, ph, nstages);
         continue;
       }
-      if (gw != 0) {
-        const RowScalars rs4 = rsc[grp];
-        g = rs4.g;
-        kscale = rs4.kscale;
-        ga = rs4.ga;
-        mL = rs4.mL;
-      } else {
-        const RowScalars rs4 = rsc[grp];
-        kscale = rs4.kscale;
-        ga = rs4.ga;
-        mL = rs4.mL;
-      }
+      rsv = rsc[grp];
     } else {
-      g = tgt_ok ? mt->g_in : 0.f;
-      mL = mt->lse_in * L2E;
-      kscale = -g;
+      const float g = tgt_ok ? mt->g_in : 0.f;
+      rsv.M = mt->lse_in;
+      rsv.k1 = -g;
+      rsv.k2 = 0.f;
+      rsv.ga = tgt_ok ? -g * expm1f(bf_lo(uint32_t(reinterpret_cast<const uint16_t*>(row)[a])) - mt->lse_in)
+                      : 0.f;
+      rsv.active = g != 0.f ? 1.f : 0.f;
     }
 
     // ---- pass C: dlogits (masked / clipped rows get exact zeros) ---------------------
     {
       __nv_bfloat16* drow = static_cast<__nv_bfloat16*>(p.dx) + int64_t(r) * p.ld;
-      // FUSED: dx = kscale 2^{(m_w - M) log2e} e  (e from pass B, bf16 in SMEM)
-      // BWD:   dx = -g 2^{(x - lse) log2e}
-      const float kw = MODE == MODE_BWD ? kscale : kscale * ex2((mws - mL) * L2E);
-      const float nmL = -mL;
+      const float kw = keep_e ? rsv.k1 * ex2((mws - rsv.M) * L2E) : rsv.k1;
+      const float nML = -rsv.M * L2E;
 #pragma unroll
       for (int i = 0; i < kVecPerThread; ++i) {
         const int idx = gt + i * kGroupThreads;
         if (idx < nvec) {
           uint4 o = make_uint4(0u, 0u, 0u, 0u);
-          if (g != 0.f) {
+          if (rsv.active != 0.f) {
             const uint4 w = rv[idx];
             const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
             uint32_t* ow = &o.x;
-            if (MODE == MODE_BWD) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                ow[q] = pack_bf16x2(kw * ex2(fmaf(bf_lo(w4[q]), L2E, nmL)),
-                                    kw * ex2(fmaf(bf_hi(w4[q]), L2E, nmL)));
-            } else {
+            if (keep_e) {
+              // FUSED: dx = g' 2^{(m_w - M) log2e} e, e from pass B (bf16 in SMEM)
 #pragma unroll
               for (int q = 0; q < 4; ++q) ow[q] = pack_bf16x2(kw * bf_lo(w4[q]), kw * bf_hi(w4[q]));
+            } else {
+              // from x: t = (x - M) log2e (lse in external bwd), dx = 2^t (k1 + k2 t);
+              // -inf columns are clamped per bf16 pair so that t stays finite
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t c = bmax2_nan(w4[q], kNegClampPair);
+                const float t0 = fmaf(bf_lo(c), L2E, nML);
+                const float t1 = fmaf(bf_hi(c), L2E, nML);
+                ow[q] = pack_bf16x2(ex2(t0) * fmaf(rsv.k2, t0, rsv.k1),
+                                    ex2(t1) * fmaf(rsv.k2, t1, rsv.k1));
+              }
             }
             if (idx == va) {
-              float dv;
-              if (MODE == MODE_BWD)
-                dv = -g * expm1f(bf_lo(uint32_t(reinterpret_cast<const uint16_t*>(row)[a])) - mt->lse_in);
-              else
-                dv = ga;
-              const uint32_t hb = uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(dv)));
+              const uint32_t hb = uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(rsv.ga)));
               const int qd = (a & 7) >> 1, hf = a & 1;
 #pragma unroll
               for (int z = 0; z < 4; ++z)
@@ -514,14 +527,14 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
 
   if (want_stats) {
     __syncthreads();
-    if (tid < 9) gacc[tid] += gacc[16 + tid];  // fixed order: group 0 then group 1
+    if (tid < kLossSlots) gacc[tid] += gacc[16 + tid];  // fixed order: group 0 then group 1
     __syncthreads();
-    finish_loss_stats(gacc, p.stats, p.partials, p.ctrl, Nden, p.accumulate);
+    finish_loss_stats(gacc, p.stats, p.partials, p.ctrl, Nden, p.accumulate, pc.ent_coef);
   }
 }
 
 // =====================================================================================
-// small V: one warp per row, register-resident
+// small V: one warp per row, register-resident (t_j kept; e recomputed in the store pass)
 // =====================================================================================
 template <typename T, int NV, int MODE>
 __global__ void __launch_bounds__(256) lp_warp_kernel(Lp p) {
@@ -532,7 +545,7 @@ __global__ void __launch_bounds__(256) lp_warp_kernel(Lp p) {
   const bool want_stats = p.stats != nullptr && MODE != MODE_BWD;
   PpoConst pc;
   const double Nden = resolve_pc<MODE>(p, pc);
-  double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double acc[kLossSlots] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   const int64_t gw = int64_t(blockIdx.x) * 8 + warp, nw = int64_t(gridDim.x) * 8;
   for (int64_t r = gw; r < p.rows; r += nw) {
     const T* xr = static_cast<const T*>(p.x) + r * p.ld;
@@ -553,12 +566,13 @@ __global__ void __launch_bounds__(256) lp_warp_kernel(Lp p) {
       }
     }
     const float xa = tgt_ok ? to_f<T>(xr[a]) : 0.f;
-    float g = 0.f, lse_row = 0.f, M = 0.f, Stot = 1.f, Srest = 0.f;
+    RowGrad rg{0.f, 0.f};
+    float Stot = 1.f, Srest = 0.f, lnS = 0.f, H = 0.f, logp = 0.f, ea = 0.f;
     if (MODE != MODE_BWD) {
       float mt = -INFINITY;
 #pragma unroll
       for (int j = 0; j < NV * VW; ++j) mt = fmaxf(mt, x[j]);
-      M = warp_max(mt);
+      const float M = warp_max(mt);
       const float Ms = (M == -INFINITY) ? 0.f : M;
       const float nmL = -Ms * L2E;
       float s = 0.f, et = 0.f;
@@ -569,7 +583,7 @@ __global__ void __launch_bounds__(256) lp_warp_kernel(Lp p) {
           const int col = (lane + 32 * i) * VW + j;
           const float t = fmaf(x[i * VW + j], L2E, nmL);
           const float ee = ex2(t);
-          x[i * VW + j] = ee;  // keep e_j in place of x_j
+          x[i * VW + j] = t;  // keep t_j = (x_j - M) log2e in place of x_j
           if (col != a) {
             s += ee;
             et = fmaf(ee, fmaxf(t, -256.f), et);
@@ -579,33 +593,33 @@ __global__ void __launch_bounds__(256) lp_warp_kernel(Lp p) {
       Srest = warp_sum(s);
       const float Cs = warp_sum(et);
       const float ta = (xa - Ms) * L2E;
-      const float ea = tgt_ok ? ex2(ta) : 0.f;
+      ea = tgt_ok ? ex2(ta) : 0.f;
       Stot = Srest + ea;
-      const float lnS = __logf(Stot);
-      lse_row = M + lnS;
-      const float logp = (xa - M) - lnS;
-      const float H = lnS - (Cs + (tgt_ok ? ea * fmaxf(ta, -256.f) : 0.f)) / (L2E * Stot);
-      float lpb = 0.f, lpp = 0.f, advv = 0.f;
-      int ver = 0;
-      uint64_t key = 1;
-      if (MODE == MODE_FUSED) {
-        const int64_t sidx = r / p.A;
-        lpb = p.lpb[r];
-        if (p.lpp) lpp = p.lpp[r];
-        advv = p.adv[sidx];
-        ver = p.ver[sidx];
-        key = p.key[sidx];
-      }
-      g = finish_row<MODE>(p, pc, r, a, lse_row, logp, H, lpb, lpp, advv, ver, key, lane == 0,
-                           want_stats ? acc : nullptr);
+      lnS = __logf(Stot);
+      const float lse_row = M + lnS;
+      logp = (xa - M) - lnS;
+      H = lnS - (Cs + (tgt_ok ? ea * fmaxf(ta, -256.f) : 0.f)) / (L2E * Stot);
+      const RowMeta rm = load_meta<MODE>(p, r);
+      rg = finish_row<MODE>(p, pc, r, a, lse_row, logp, H, rm, lane == 0,
+                            want_stats ? acc : nullptr);
     } else {
-      g = tgt_ok ? p.g_in[r] : 0.f;
-      lse_row = p.lse_in[r];
+      rg.g = tgt_ok ? p.g_in[r] : 0.f;
+      const float lse_row = p.lse_in[r];
+      const float off = lse_row * L2E;
+      logp = xa - lse_row;
+#pragma unroll
+      for (int j = 0; j < NV * VW; ++j) x[j] = fmaf(x[j], L2E, -off);  // t relative to lse
     }
     if (p.dx != nullptr && MODE != MODE_FWD) {
       T* dr = static_cast<T*>(p.dx) + r * p.ld;
       const float invS = 1.f / Stot;
-      const float nlL = -lse_row * L2E;
+      // dx_j = 2^{t_j} (k1 + k2 t_j): FUSED k1 = (-g + c (H - lnS)) / S, k2 = c ln2 / S;
+      //                               BWD   k1 = -g, k2 = 0 (t relative to lse)
+      const float k1 = MODE == MODE_BWD ? -rg.g : (-rg.g + rg.c * (H - lnS)) * invS;
+      const float k2 = MODE == MODE_BWD ? 0.f : rg.c * kLn2 * invS;
+      const float ga = MODE == MODE_BWD ? -rg.g * expm1f(logp)
+                                        : target_grad(rg, Srest, ea, invS, logp, H);
+      const bool active = rg.g != 0.f || rg.c != 0.f;
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
         const int idx = lane + 32 * i;
@@ -615,15 +629,9 @@ __global__ void __launch_bounds__(256) lp_warp_kernel(Lp p) {
 #pragma unroll
           for (int j = 0; j < VW; ++j) {
             const int col = idx * VW + j;
-            float d;
-            if (g == 0.f) {
-              d = 0.f;
-            } else if (MODE == MODE_BWD) {
-              d = (col == a) ? -g * expm1f(x[i * VW + j] - lse_row)
-                             : -g * ex2(fmaf(x[i * VW + j], L2E, nlL));
-            } else {
-              d = (col == a) ? g * Srest * invS : -g * x[i * VW + j] * invS;
-            }
+            const float t = clamp_ninf(x[i * VW + j]);
+            float d = 0.f;
+            if (active) d = (col == a) ? ga : ex2(t) * fmaf(k2, t, k1);
             tv[j] = from_f<T>(d);
           }
           stg_stream(reinterpret_cast<uint4*>(dr) + idx, u);
@@ -632,18 +640,18 @@ __global__ void __launch_bounds__(256) lp_warp_kernel(Lp p) {
     }
   }
   if (want_stats) {
-    __shared__ double red[8][9];
-    __shared__ double cta[9];
+    __shared__ double red[8][kLossSlots];
+    __shared__ double cta[kLossSlots];
     if (lane == 0)
-      for (int k = 0; k < 9; ++k) red[warp][k] = acc[k];
+      for (int k = 0; k < kLossSlots; ++k) red[warp][k] = acc[k];
     __syncthreads();
-    if (threadIdx.x < 9) {
+    if (threadIdx.x < kLossSlots) {
       double s = 0;
       for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
       cta[threadIdx.x] = s;
     }
     __syncthreads();
-    finish_loss_stats(cta, p.stats, p.partials, p.ctrl, Nden, p.accumulate);
+    finish_loss_stats(cta, p.stats, p.partials, p.ctrl, Nden, p.accumulate, pc.ent_coef);
   }
 }
 
@@ -667,7 +675,8 @@ __global__ void __launch_bounds__(256) lp_generic_kernel(Lp p) {
     const int a = p.target[r];
     const bool tgt_ok = unsigned(a) < unsigned(V);
     const float xa = tgt_ok ? to_f<T>(xr[a]) : 0.f;
-    float g, lse_row, Stot = 1.f, Srest = 0.f, Ms = 0.f;
+    RowGrad rg{0.f, 0.f};
+    float Stot = 1.f, Srest = 0.f, Ms = 0.f, lnS = 0.f, H = 0.f, logp = 0.f, ea = 0.f, lse_row;
     if (MODE != MODE_BWD) {
       float mt = -INFINITY;
       for (int j = tid; j < V; j += 256) mt = fmaxf(mt, to_f<T>(xr[j]));
@@ -701,42 +710,32 @@ __global__ void __launch_bounds__(256) lp_generic_kernel(Lp p) {
         Cs += redf[1][w];
       }
       const float ta = (xa - Ms) * L2E;
-      const float ea = tgt_ok ? ex2(ta) : 0.f;
+      ea = tgt_ok ? ex2(ta) : 0.f;
       Stot = Srest + ea;
-      const float lnS = __logf(Stot);
+      lnS = __logf(Stot);
       lse_row = M + lnS;
-      const float logp = (xa - M) - lnS;
-      const float H = lnS - (Cs + (tgt_ok ? ea * fmaxf(ta, -256.f) : 0.f)) / (L2E * Stot);
-      float lpb = 0.f, lpp = 0.f, advv = 0.f;
-      int ver = 0;
-      uint64_t key = 1;
-      if (MODE == MODE_FUSED) {
-        const int64_t sidx = r / p.A;
-        lpb = p.lpb[r];
-        if (p.lpp) lpp = p.lpp[r];
-        advv = p.adv[sidx];
-        ver = p.ver[sidx];
-        key = p.key[sidx];
-      }
-      g = finish_row<MODE>(p, pc, r, a, lse_row, logp, H, lpb, lpp, advv, ver, key, tid == 0,
-                           want_stats ? sacc : nullptr);
+      logp = (xa - M) - lnS;
+      H = lnS - (Cs + (tgt_ok ? ea * fmaxf(ta, -256.f) : 0.f)) / (L2E * Stot);
+      const RowMeta rm = load_meta<MODE>(p, r);
+      rg = finish_row<MODE>(p, pc, r, a, lse_row, logp, H, rm, tid == 0, want_stats ? sacc : nullptr);
     } else {
-      g = tgt_ok ? p.g_in[r] : 0.f;
+      rg.g = tgt_ok ? p.g_in[r] : 0.f;
       lse_row = p.lse_in[r];
+      logp = xa - lse_row;
     }
     if (p.dx != nullptr && MODE != MODE_FWD) {
       T* dr = static_cast<T*>(p.dx) + r * p.ld;
       const float invS = 1.f / Stot;
-      const float nmL = -Ms * L2E, nlL = -lse_row * L2E;
+      const float off = MODE == MODE_BWD ? lse_row * L2E : Ms * L2E;
+      const float k1 = MODE == MODE_BWD ? -rg.g : (-rg.g + rg.c * (H - lnS)) * invS;
+      const float k2 = MODE == MODE_BWD ? 0.f : rg.c * kLn2 * invS;
+      const float ga = MODE == MODE_BWD ? -rg.g * expm1f(logp)
+                                        : target_grad(rg, Srest, ea, invS, logp, H);
+      const bool active = rg.g != 0.f || rg.c != 0.f;
       for (int j = tid; j < V; j += 256) {
-        const float xj = to_f<T>(xr[j]);
-        float d;
-        if (g == 0.f) d = 0.f;
-        else if (MODE == MODE_BWD) {
-          d = (j == a) ? -g * expm1f(xj - lse_row) : -g * ex2(fmaf(xj, L2E, nlL));
-        } else {
-          d = (j == a) ? g * Srest * invS : -g * ex2(fmaf(xj, L2E, nmL)) * invS;
-        }
+        const float t = clamp_ninf(fmaf(to_f<T>(xr[j]), L2E, -off));
+        float d = 0.f;
+        if (active) d = (j == a) ? ga : ex2(t) * fmaf(k2, t, k1);
         dr[j] = from_f<T>(d);
       }
     }
@@ -744,7 +743,7 @@ __global__ void __launch_bounds__(256) lp_generic_kernel(Lp p) {
   }
   if (want_stats) {
     __syncthreads();
-    finish_loss_stats(sacc, p.stats, p.partials, p.ctrl, Nden, p.accumulate);
+    finish_loss_stats(sacc, p.stats, p.partials, p.ctrl, Nden, p.accumulate, pc.ent_coef);
   }
 }
 
@@ -766,16 +765,21 @@ Lp make_lp(const LpArgs& a) {
   if (a.fused) {
     p.lpb = a.f.logp_behav;
     p.lpp = a.f.logp_prox;
+    p.lref = (a.f.logp_ref != nullptr && a.f.kl_coef != 0.f) ? a.f.logp_ref : nullptr;
     p.adv = a.f.adv;
     p.ver = a.f.version;
     p.key = a.f.slot_key;
     p.A = a.f.a_tok;
     p.pc.has_prox = a.f.logp_prox != nullptr;
+    p.pc.has_ref = p.lref != nullptr;
     p.pc.cur_version = a.f.cur_version;
     p.pc.eta = a.f.max_staleness;
     p.pc.lo = 1.f - a.f.eps_low;
     p.pc.hi = 1.f + a.f.eps_high;
     p.pc.is_cap = a.f.is_cap;
+    p.pc.dual_clip = a.f.dual_clip;
+    p.pc.kl_coef = a.f.kl_coef;
+    p.pc.ent_coef = a.f.ent_coef;
     p.out_g = a.f.out_grad_logp;
     p.out_L = a.f.out_loss_tok;
     p.accumulate = a.f.accumulate;

@@ -1,18 +1,37 @@
-// ppo.cu — S4 over precomputed log-probs (rlvla_ppo_loss, K8): the same per-row epilogue
-// as the fused log-prob kernels (epilogue.cuh), one thread per row, fp64 per-CTA partials
-// summed in fixed order by the last CTA. See epilogue.cuh for the definition and the
-// paper anchors (P:62 staleness, P:18 decoupled objective).
+// ppo.cu — S4 over precomputed log-probs (rlvla_ppo_loss, K8) and the clipped value loss
+// (rlvla_value_loss). The token-level path uses the same per-row epilogue as the fused
+// log-prob kernels (epilogue.cuh): one thread per row, fp64 per-CTA partials summed in
+// fixed order by the last CTA. The chunk-level path (ratio_level = 1, reading R21) gives
+// each decision step one ratio exp(sum_a m (logp - logp_behav)): one warp per step.
+// Paper anchors: P:62 (staleness), P:18 (decoupled objective), P:99 (action chunks).
 #include "epilogue.cuh"
 
 namespace rlvla {
 namespace {
 
-__global__ void __launch_bounds__(256) ppo_loss_kernel(PpoArgs a, PpoConst pc0) {
+__device__ __forceinline__ void block_finish(double* acc, int nslot, const PpoArgs& a,
+                                             unsigned* ctrl, double N, float ent_coef) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ double red[8][kLossSlots];
+  __shared__ double cta[kLossSlots];
+  for (int k = 0; k < nslot; ++k) acc[k] = warp_sum_d(acc[k]);
+  if (lane == 0)
+    for (int k = 0; k < nslot; ++k) red[warp][k] = acc[k];
+  __syncthreads();
+  if (threadIdx.x < nslot) {
+    double s = 0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) s += red[w][threadIdx.x];
+    cta[threadIdx.x] = s;
+  }
+  __syncthreads();
+  finish_loss_stats(cta, a.stats, a.ws.partials, ctrl, N, a.f.accumulate, ent_coef);
+}
+
+__global__ void __launch_bounds__(256) ppo_loss_kernel(PpoArgs a, PpoConst pc0) {
   PpoConst pc = pc0;
   const double N = loss_denominator(a.f.tok_denominator, a.f.adv_stats);
   pc.invN = N > 0.0 ? float(1.0 / N) : 0.f;
-  double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double acc[kLossSlots] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   const int A = a.f.a_tok;
   for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < a.rows;
        r += int64_t(gridDim.x) * blockDim.x) {
@@ -24,6 +43,7 @@ __global__ void __launch_bounds__(256) ppo_loss_kernel(PpoArgs a, PpoConst pc0) 
     in.H = 0.f;
     in.lpb = a.f.logp_behav[r];
     in.lpp = a.f.logp_prox ? a.f.logp_prox[r] : 0.f;
+    in.lref = pc.has_ref ? a.f.logp_ref[r] : 0.f;
     const int64_t s = r / A;
     in.adv = a.f.adv[s];
     in.ver = a.f.version[s];
@@ -36,20 +56,120 @@ __global__ void __launch_bounds__(256) ppo_loss_kernel(PpoArgs a, PpoConst pc0) 
     acc_stats(acc, rs);
   }
   if (a.stats == nullptr) return;
-  __shared__ double red[8][9];
-  __shared__ double cta[9];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) acc[k] = warp_sum_d(acc[k]);
-  if (lane == 0)
-    for (int k = 0; k < 9; ++k) red[warp][k] = acc[k];
-  __syncthreads();
-  if (threadIdx.x < 9) {
-    double s = 0;
-    for (int w = 0; w < int(blockDim.x >> 5); ++w) s += red[w][threadIdx.x];
-    cta[threadIdx.x] = s;
+  block_finish(acc, kLossSlots, a, a.ws.ctrl + CTRL_PPO, N, 0.f);
+}
+
+// Chunk-level ratio: warp per decision step s. m_a = valid [usable] [0 <= lag <= eta];
+// lr_s = sum_a m_a (logp_a - logp_behav_a) (fixed xor-tree order); rho_s = e^{lr_s};
+// L_s = -min(rho A, clip(rho) A) on steps with >= 1 masked token, Loss = sum L_s / N_steps;
+// grad = -A rho [active] / N_steps on every masked token of the step (scaled by the second
+// kernel once N_steps is known); loss_tok = L_s / n_tok(s) on the step's masked tokens.
+// Stats: LOSS = PG_LOSS, N_CLIPPED / KL_K3_SUM / RATIO_SUM per step, N_LOSS_TOK,
+// N_STALE_TOK, N_BAD_TOK, LOGP_SUM per token; DENOM = N_steps.
+__device__ __forceinline__ int tok_status(const PpoArgs& a, int64_t r, float lp) {
+  const int t = a.target ? a.target[r] : 0;
+  return (t == -1) ? 1 : (t < -1 ? 2 : (isfinite(lp) ? 0 : 3));
+}
+
+__device__ __forceinline__ double* chunk_scratch(const PpoArgs& a) {
+  return reinterpret_cast<double*>(a.ws.ctrl + 32);  // 1/N_steps for the scale pass
+}
+
+__global__ void __launch_bounds__(256) ppo_chunk_kernel(PpoArgs a, PpoConst pc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int A = a.f.a_tok;
+  const int64_t S = a.rows / A;
+  const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  double acc[kLossSlots] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int64_t s = gw; s < S; s += nw) {
+    const bool valid = a.f.slot_key[s] != 0ull;
+    const int lag = pc.cur_version - a.f.version[s];
+    const bool step_ok = valid && lag >= 0 && lag <= pc.eta;
+    float lr = 0.f, ntok = 0.f, nstale = 0.f, nbad = 0.f, lps = 0.f;
+    for (int j = lane; j < A; j += 32) {
+      const int64_t r = s * A + j;
+      const float lp = a.logp[r];
+      const int stt = tok_status(a, r, lp);
+      const bool usable = valid && stt == 0;
+      if (usable && step_ok) {
+        lr += lp - a.f.logp_behav[r];
+        ntok += 1.f;
+        lps += lp;
+      }
+      if (usable && lag > pc.eta) nstale += 1.f;
+      if ((valid && (stt == 2 || stt == 3)) || (usable && lag < 0)) nbad += 1.f;
+    }
+    lr = warp_sum(lr);
+    ntok = warp_sum(ntok);
+    nstale = warp_sum(nstale);
+    nbad = warp_sum(nbad);
+    lps = warp_sum(lps);
+    const float rho = __expf(lr);
+    const float Aa = a.f.adv[s];
+    const float rc = fminf(fmaxf(rho, pc.lo), pc.hi);
+    const float J = fminf(rho * Aa, rc * Aa);
+    const bool clipped = (Aa > 0.f && rho > pc.hi) || (Aa < 0.f && rho < pc.lo);
+    const bool has = ntok > 0.f;
+    const float gs = (has && !clipped) ? -Aa * rho : 0.f;
+    const float lt = has ? -J / ntok : 0.f;
+    for (int j = lane; j < A; j += 32) {
+      const int64_t r = s * A + j;
+      const bool m = step_ok && tok_status(a, r, a.logp[r]) == 0;
+      a.grad_logp[r] = m ? gs : 0.f;
+      if (a.loss_tok) a.loss_tok[r] = m ? lt : 0.f;
+    }
+    if (lane == 0) {
+      if (has) {
+        acc[0] += double(-J);
+        acc[11] += double(-J);
+        acc[1] += clipped ? 1.0 : 0.0;
+        acc[2] += double(fabsf(lr) < 0.125f
+                             ? lr * lr * (0.5f + lr * (1.f / 6.f + lr * (1.f / 24.f + lr * (1.f / 120.f + lr * (1.f / 720.f)))))
+                             : (rho - 1.f - lr));
+        acc[4] += double(rho);
+        acc[9] += 1.0;  // number of loss steps (-> DENOM, slot zeroed below)
+      }
+      acc[5] += double(ntok);
+      acc[6] += double(nstale);
+      acc[7] += double(nbad);
+      acc[8] += double(lps);
+    }
   }
+  __shared__ double red[8][kLossSlots];
+  for (int k = 0; k < kLossSlots; ++k) acc[k] = warp_sum_d(acc[k]);
+  if (lane == 0)
+    for (int k = 0; k < kLossSlots; ++k) red[warp][k] = acc[k];
   __syncthreads();
-  finish_loss_stats(cta, a.stats, a.ws.partials, a.ws.ctrl + CTRL_PPO, N, a.f.accumulate);
+  if (threadIdx.x < kLossSlots) {
+    double sum = 0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) sum += red[w][threadIdx.x];
+    a.ws.partials[size_t(blockIdx.x) * RLVLA_NSTATS + threadIdx.x] = sum;
+  }
+  __shared__ double tot[kLossSlots];
+  if (last_block_reduce(a.ws.ctrl + CTRL_PPO, a.ws.partials, kLossSlots, tot)) {
+    const double Ns = a.f.tok_denominator > 0.0 ? a.f.tok_denominator : tot[9];
+    const double inv = Ns > 0.0 ? 1.0 / Ns : 0.0;
+    if (threadIdx.x < kLossSlots && a.stats) {
+      double v = tot[threadIdx.x];
+      if (threadIdx.x == 0 || threadIdx.x == 11) v *= inv;
+      if (threadIdx.x == 9) v = 0.0;  // KL_REF_SUM: no reference term on this path
+      if (a.f.accumulate) v += a.stats[RLVLA_STAT_LOSS + threadIdx.x];
+      a.stats[RLVLA_STAT_LOSS + threadIdx.x] = v;
+    }
+    if (threadIdx.x == 0) {
+      if (a.stats) a.stats[RLVLA_STAT_DENOM] = Ns;
+      *chunk_scratch(a) = inv;
+    }
+  }
+}
+
+// second pass of the chunk path: scale the per-token step gradients by 1/N_steps
+__global__ void __launch_bounds__(256) ppo_chunk_scale_kernel(PpoArgs a) {
+  const float fi = float(*chunk_scratch(a));
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < a.rows;
+       r += int64_t(gridDim.x) * blockDim.x)
+    a.grad_logp[r] *= fi;
 }
 
 }  // namespace
@@ -58,13 +178,31 @@ cudaError_t launch_ppo_loss(const PpoArgs& a, cudaStream_t s) {
   if (a.rows <= 0) return cudaSuccess;
   PpoConst pc{};
   pc.has_prox = a.f.logp_prox != nullptr;
+  pc.has_ref = a.f.logp_ref != nullptr && a.f.kl_coef != 0.f;
   pc.cur_version = a.f.cur_version;
   pc.eta = a.f.max_staleness;
   pc.lo = 1.f - a.f.eps_low;
   pc.hi = 1.f + a.f.eps_high;
   pc.is_cap = a.f.is_cap;
+  pc.dual_clip = a.f.dual_clip;
+  pc.kl_coef = a.f.kl_coef;
+  pc.ent_coef = 0.f;  // no logits here: the entropy bonus lives in the logits path
+  const int sms = device_info().sm_count;
+  if (a.f.ratio_level == 1) {
+    const int64_t S = a.rows / a.f.a_tok;
+    int64_t blocks = (S + 7) / 8;
+    if (blocks > int64_t(sms) * 4) blocks = int64_t(sms) * 4;
+    if (blocks < 1) blocks = 1;
+    ppo_chunk_kernel<<<int(blocks), 256, 0, s>>>(a, pc);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    int64_t b2 = (a.rows + 255) / 256;
+    if (b2 > int64_t(sms) * 4) b2 = int64_t(sms) * 4;
+    ppo_chunk_scale_kernel<<<int(b2), 256, 0, s>>>(a);
+    return cudaGetLastError();
+  }
   int64_t blocks = (a.rows + 255) / 256;
-  const int64_t cap = int64_t(device_info().sm_count) * 4;
+  const int64_t cap = int64_t(sms) * 4;
   if (blocks > cap) blocks = cap;
   ppo_loss_kernel<<<int(blocks), 256, 0, s>>>(a, pc);
   return cudaGetLastError();

@@ -27,7 +27,7 @@ def full():
     obuf, ocnt = H.oracle_scatter(case)
     E, T, A, V = cfg.n_env, cfg.t_steps, cfg.a_tok, cfg.vocab
     ws = P.workspace(E)
-    stats = torch.zeros(16, dtype=torch.float64, device="cuda")
+    stats = torch.zeros(24, dtype=torch.float64, device="cuda")
     adv = torch.zeros(E, T, device="cuda")
     ret = torch.zeros(E, T, device="cuda")
     prm = P.adv_params("grpo", group_id=torch.from_numpy(case.traj.group_id).cuda(), group_size=8,
@@ -39,7 +39,7 @@ def full():
     g = torch.empty(R, device="cuda")
     lt = torch.empty(R, device="cuda")
     dx = torch.empty_like(case.logits)
-    st2 = torch.zeros(16, dtype=torch.float64, device="cuda")
+    st2 = torch.zeros(24, dtype=torch.float64, device="cuda")
     fa = P.ppo_args(logp_behav=gbuf.logp_behav.view(-1), adv=adv.view(-1), version=gbuf.version.view(-1),
                     slot_key=gbuf.slot_key.view(-1), a_tok=A, cur_version=synth.CUR_VERSION,
                     adv_stats=stats, out_grad_logp=g, out_loss_tok=lt)
@@ -100,7 +100,7 @@ def test_fullsize_properties(full):
     N = full["stats"][3].item()
     lt = full["lt"].double().sum().item()
     assert abs(st[6] - lt / N) <= 1e-9 * max(1.0, abs(lt / N)) + 1e-12
-    assert st[15] == N
+    assert st[18] == N
     mask = full["g"] != 0
     assert st[11] >= mask.sum().item()
 
@@ -110,7 +110,7 @@ def test_fullsize_rerun_bit_identical(full):
     case = full["case"]
     dx2 = torch.empty_like(full["dx"])
     logp2 = torch.empty_like(full["logp"])
-    st = torch.zeros(16, dtype=torch.float64, device="cuda")
+    st = torch.zeros(24, dtype=torch.float64, device="cuda")
     P.rlvla_logprob_fwd_bwd(case.logits, full["gbuf"].tokens.view(-1), logp=logp2, fused=full["fa"],
                             dlogits=dx2, stats=st, ws=full["ws"])
     torch.cuda.synchronize()

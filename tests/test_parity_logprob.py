@@ -78,7 +78,7 @@ def test_forward_and_external_backward(R, V, dtype, path):
     tgt = torch.from_numpy(t).cuda()
     logp = torch.full((R,), 123.0, device="cuda")
     lse = torch.empty(R, device="cuda")
-    stats = torch.zeros(16, dtype=torch.float64, device="cuda")
+    stats = torch.zeros(24, dtype=torch.float64, device="cuda")
     ws = P.workspace(1)
     P.rlvla_logprob_fwd_bwd(x, tgt, logp=logp, lse=lse, stats=stats, ws=ws)
     x64 = x.double().cpu().numpy()
@@ -148,7 +148,7 @@ def test_fused_ppo(R, V, dtype, path, decoupled):
     lt = torch.empty(R, device="cuda")
     logp = torch.empty(R, device="cuda")
     dx = torch.empty_like(x)
-    stats = torch.zeros(16, dtype=torch.float64, device="cuda")
+    stats = torch.zeros(24, dtype=torch.float64, device="cuda")
     ws = P.workspace(1)
     N = 1000.0
     fa = P.ppo_args(logp_behav=cuda(lb), logp_prox=cuda(lpp) if decoupled else None,
@@ -178,11 +178,11 @@ def test_fused_ppo(R, V, dtype, path, decoupled):
     assert abs(st[10] - s["ratio_sum"]) <= 1e-5 * max(1.0, s["ratio_sum"])
     ent = np.where(o["mask"], f["entropy"], 0).sum()
     assert abs(st[9] - ent) <= 1e-5 * max(1.0, abs(ent))
-    assert st[15] == N
+    assert st[18] == N
     # the same epilogue through rlvla_ppo_loss on the GPU log-probs (fused == unfused)
     g2 = torch.empty(R, device="cuda")
     lt2 = torch.empty(R, device="cuda")
-    st2 = torch.zeros(16, dtype=torch.float64, device="cuda")
+    st2 = torch.zeros(24, dtype=torch.float64, device="cuda")
     tg = cuda(np.where((t >= 0) & (t < V), t, np.where(t == -1, -1, -2)).astype(np.int32))
     P.rlvla_ppo_loss(logp, tg, fa, g2, lt2, st2, ws)
     assert torch.equal(g2, g) and torch.equal(lt2, lt)
@@ -204,7 +204,7 @@ def test_in_place_dlogits_and_determinism():
     for _ in range(2):
         logp = torch.empty(R, device="cuda")
         dx = torch.empty_like(x)
-        st = torch.zeros(16, dtype=torch.float64, device="cuda")
+        st = torch.zeros(24, dtype=torch.float64, device="cuda")
         P.rlvla_logprob_fwd_bwd(x, t, logp=logp, fused=fa, dlogits=dx, stats=st, ws=P.workspace(1))
         outs.append((logp, dx, st))
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
@@ -246,7 +246,7 @@ def test_ratio_one_pin_through_gpu():
     key = torch.ones(R // A, dtype=torch.int64, device="cuda")
     ver = torch.full((R // A,), 100, dtype=torch.int32, device="cuda")
     g = torch.empty(R, device="cuda")
-    st = torch.zeros(16, dtype=torch.float64, device="cuda")
+    st = torch.zeros(24, dtype=torch.float64, device="cuda")
     fa = P.ppo_args(logp_behav=lp0, adv=cuda(adv), version=ver, slot_key=key, a_tok=A,
                     cur_version=100, tok_denominator=float(R), out_grad_logp=g)
     P.rlvla_logprob_fwd_bwd(x, t, logp=torch.empty(R, device="cuda"), fused=fa,

@@ -1,0 +1,205 @@
+"""GPU parity for the NEXT-2 loss variants (paper-silent; readings R19-R23) against the oracle:
+dual-clip, reference-KL (k3), entropy bonus (gradient through the logits) on all three
+log-prob kernel paths; chunk-level ratio and token-level variants through rlvla_ppo_loss;
+the clipped value loss; GAE with time-limit truncation."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import advantages as O_adv
+from oracle import logprob as O_lp
+from oracle import path as O_path
+from oracle import ppo as O_ppo
+from tests import harness as H
+
+pytestmark = pytest.mark.gpu
+
+
+def _P():
+    import paper_2602_05765_b200 as P
+    return P
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _case(R, V, dtype, A, seed=0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    x = (torch.randn(R, V, generator=g) * 1.5)
+    x[1] = -30.0
+    x[1, 3] = 30.0                                   # saturated row (target 3)
+    x[2, [1, 2, V // 2]] = float("-inf")             # -inf columns (target 0)
+    x = x.to(dtype)
+    rng = np.random.default_rng(seed)
+    t = rng.integers(0, V, R).astype(np.int32)
+    t[1], t[2], t[4] = 3, 0, -1
+    x64 = x.double().numpy()
+    f = O_lp.log_softmax_gather(x64, t)
+    lp = np.nan_to_num(f["logp"])
+    lr = rng.choice([-1.3, -0.4, -0.05, 0.03, 0.1, 0.4, 1.4], R) + rng.normal(0, 0.01, R)
+    lb = (lp - lr).astype(np.float32)
+    lref = (lp + rng.normal(0, 0.3, R)).astype(np.float32)
+    S = R // A
+    adv = rng.normal(size=S).astype(np.float32)
+    ver = (100 - rng.choice([0, 1, 2], size=S, p=[0.6, 0.3, 0.1])).astype(np.int32)
+    key = np.where(rng.random(S) < 0.95, 7, 0).astype(np.int64)
+    return x, t, x64, f, lb, lref, adv, ver, key
+
+
+VARIANTS = [dict(dual_clip=3.0), dict(kl_coef=0.05), dict(ent_coef=0.01),
+            dict(dual_clip=2.5, kl_coef=0.1, ent_coef=0.02)]
+SHAPES = [(280, 256, torch.float32), (280, 1000, torch.bfloat16), (140, 32000, torch.bfloat16),
+          (56, 5003, torch.float32)]
+
+
+@pytest.mark.parametrize("R,V,dtype", SHAPES)
+@pytest.mark.parametrize("var", VARIANTS)
+def test_fused_variants(R, V, dtype, var):
+    P = _P()
+    A = 7
+    x, t, x64, f, lb, lref, adv, ver, key = _case(R, V, dtype, A)
+    N = 250.0
+    g = torch.empty(R, device="cuda")
+    lt = torch.empty(R, device="cuda")
+    logp = torch.empty(R, device="cuda")
+    xd = x.cuda()
+    dx = torch.empty_like(xd)
+    st = torch.zeros(24, dtype=torch.float64, device="cuda")
+    fa = P.ppo_args(logp_behav=_cuda(lb), adv=_cuda(adv), version=_cuda(ver), slot_key=_cuda(key),
+                    a_tok=A, cur_version=100, tok_denominator=N, out_grad_logp=g, out_loss_tok=lt,
+                    logp_ref=_cuda(lref) if var.get("kl_coef") else None, **var)
+    P.rlvla_logprob_fwd_bwd(xd, _cuda(t), logp=logp, fused=fa, dlogits=dx, stats=st, ws=P.workspace(1))
+    valid = np.repeat(key != 0, A)
+    lag = np.repeat(100 - ver.astype(np.int64), A)
+    tv = dict(valid=valid, lag=lag, adv=np.repeat(adv, A).astype(np.float64), target=t, logp_behav=lb)
+    ref = O_path.loss_and_grad(x64, tv, n_tok=N, dual_clip=var.get("dual_clip", 0.0),
+                               logp_ref=lref if var.get("kl_coef") else None,
+                               kl_coef=var.get("kl_coef", 0.0), ent_coef=var.get("ent_coef", 0.0))
+    p, rs = ref["ppo"], ref["stats"]
+    nt = p["near_tie"]
+    H.assert_close_rel(logp.cpu().numpy(), ref["fwd"]["logp"], 1e-5, 1.0, "logp")
+    H.assert_close_rel(g.cpu().numpy()[~nt], p["grad"][~nt], 1e-5, 1e-7, "grad_logp")
+    H.assert_close_rel(lt.cpu().numpy()[~nt], p["loss_tok"][~nt], 1e-5, 1e-4, "loss_tok")
+    d = dx.cpu()
+    if dtype == torch.bfloat16:
+        bits = d.view(torch.int16).numpy().astype(np.int32) & 0xFFFF
+        H.assert_bf16_ulp(bits[~nt], ref["dx"][~nt], 1)
+    else:
+        rsc = np.abs(ref["dx"]).max(axis=1, keepdims=True)
+        H.assert_close_rel(d.numpy()[~nt], ref["dx"][~nt], 1e-5, np.maximum(rsc[~nt] * 1e-6, 1e-30), "dx")
+    s = st.cpu().numpy()
+    tol = lambda v: 1e-5 * max(1e-3, abs(v)) + 1e-6  # noqa: E731
+    assert abs(s[6] - rs["loss"]) <= tol(rs["loss"]), (s[6], rs["loss"])
+    assert abs(s[17] - rs["pg_loss"]) <= tol(rs["pg_loss"])
+    assert abs(s[15] - rs["kl_ref_sum"]) <= tol(rs["kl_ref_sum"])
+    assert abs(s[16] - rs["n_dual_clipped"]) <= nt.sum()
+    assert abs(s[9] - rs["entropy_sum"]) <= tol(rs["entropy_sum"])
+    assert s[11] == rs["n_loss_tok"] and s[18] == N
+
+
+@pytest.mark.parametrize("var", [dict(), dict(dual_clip=3.0), dict(kl_coef=0.2)])
+def test_ppo_loss_token_variants(var):
+    P = _P()
+    R, A = 700, 7
+    rng = np.random.default_rng(1)
+    logp = rng.normal(-4, 1, R).astype(np.float32)
+    lb = (logp - rng.choice([-1.3, -0.1, 0.05, 1.4], R) - rng.normal(0, 0.01, R)).astype(np.float32)
+    lref = (logp + rng.normal(0, 0.3, R)).astype(np.float32)
+    adv = rng.normal(size=R // A).astype(np.float32)
+    ver = np.full(R // A, 100, np.int32)
+    key = np.ones(R // A, np.int64)
+    g = torch.empty(R, device="cuda")
+    st = torch.zeros(24, dtype=torch.float64, device="cuda")
+    fa = P.ppo_args(logp_behav=_cuda(lb), adv=_cuda(adv), version=_cuda(ver), slot_key=_cuda(key),
+                    a_tok=A, cur_version=100, tok_denominator=float(R),
+                    logp_ref=_cuda(lref) if var.get("kl_coef") else None, **var)
+    P.rlvla_ppo_loss(_cuda(logp), None, fa, g, None, st, P.workspace(1))
+    o = O_ppo.ppo_loss(logp, lb, np.repeat(adv, A), np.ones(R, bool), np.zeros(R, int),
+                       n_tok=float(R), dual_clip=var.get("dual_clip", 0.0),
+                       logp_ref=lref if var.get("kl_coef") else None, kl_coef=var.get("kl_coef", 0.0))
+    nt = o["near_tie"]
+    H.assert_close_rel(g.cpu().numpy()[~nt], o["grad"][~nt], 1e-5, 1e-9, "grad")
+    s = st.cpu().numpy()
+    assert abs(s[6] - o["stats"]["loss"]) <= 1e-5 * abs(o["stats"]["loss"]) + 1e-7
+
+
+def test_ppo_loss_chunk_ratio():
+    P = _P()
+    S, A = 300, 56
+    R = S * A
+    rng = np.random.default_rng(2)
+    logp = rng.normal(-4, 1, R).astype(np.float32)
+    lb = (logp - rng.normal(0, 0.004, R)).astype(np.float32)     # step ratios ~ e^{N(0, 0.03)}
+    t = np.where(rng.random(R) < 0.03, -1, 5).astype(np.int32)
+    adv = rng.normal(size=S).astype(np.float32)
+    ver = (100 - rng.choice([0, 1, 2], size=S, p=[0.7, 0.2, 0.1])).astype(np.int32)
+    key = np.where(rng.random(S) < 0.95, 3, 0).astype(np.int64)
+    g = torch.empty(R, device="cuda")
+    lt = torch.empty(R, device="cuda")
+    st = torch.zeros(24, dtype=torch.float64, device="cuda")
+    fa = P.ppo_args(logp_behav=_cuda(lb), adv=_cuda(adv), version=_cuda(ver), slot_key=_cuda(key),
+                    a_tok=A, cur_version=100, ratio_level=1)
+    P.rlvla_ppo_loss(_cuda(logp), _cuda(t), fa, g, lt, st, P.workspace(1))
+    lag = np.repeat(100 - ver.astype(np.int64), A)
+    m = np.repeat(key != 0, A) & (t >= 0) & (lag >= 0) & (lag <= 1)
+    o = O_ppo.ppo_loss_chunk(logp, lb, adv, m, np.arange(R) // A, S)
+    near = np.abs(o["rho_step"] / 1.2 - 1) < 1e-5
+    near |= np.abs(o["rho_step"] / 0.8 - 1) < 1e-5
+    okt = ~np.repeat(near, A)
+    H.assert_close_rel(g.cpu().numpy()[okt], o["grad"][okt], 1e-5, 1e-9, "chunk grad")
+    s = st.cpu().numpy()
+    assert abs(s[6] - o["stats"]["loss"]) <= 1e-5 * abs(o["stats"]["loss"]) + 1e-7
+    assert s[18] == o["stats"]["n_steps"] and s[11] == m.sum()
+    assert abs(lt.double().sum().item() - o["loss_step"].sum()) <= 1e-4 * abs(o["loss_step"].sum()) + 1e-5
+
+
+@pytest.mark.parametrize("clip_eps,denom", [(0.2, 0.0), (0.0, 0.0), (0.5, 1234.0)])
+def test_value_loss(clip_eps, denom):
+    P = _P()
+    n = 5000
+    rng = np.random.default_rng(3)
+    v, vo, R = (rng.normal(size=n).astype(np.float32) for _ in range(3))
+    key = np.where(rng.random(n) < 0.9, 1, 0).astype(np.int64)
+    ver = (100 - rng.choice([0, 1, 2], size=n, p=[0.7, 0.2, 0.1])).astype(np.int32)
+    gv = torch.empty(n, device="cuda")
+    ls = torch.empty(n, device="cuda")
+    st = torch.zeros(24, dtype=torch.float64, device="cuda")
+    P.rlvla_value_loss(_cuda(v), _cuda(vo), _cuda(R), _cuda(key), _cuda(ver), 100, gv,
+                       clip_eps=clip_eps, denominator=denom, loss_step=ls, stats=st, ws=P.workspace(1))
+    lag = 100 - ver.astype(np.int64)
+    m = (key != 0) & (lag >= 0) & (lag <= 1)
+    o = O_ppo.value_loss(v, vo, R, m, clip_eps=clip_eps, n_den=denom if denom > 0 else None)
+    d = np.abs(v.astype(np.float64) - vo)
+    ok = np.abs(d - clip_eps) > 1e-5 if clip_eps > 0 else np.ones(n, bool)
+    H.assert_close_rel(gv.cpu().numpy()[ok], o["grad"][ok], 1e-5, 1e-9, "value grad")
+    s = st.cpu().numpy()
+    assert abs(s[19] - o["stats"]["loss"]) <= 1e-5 * o["stats"]["loss"]
+    assert s[21] == m.sum() and s[22] == o["stats"]["denom"]
+    assert abs(s[20] - o["stats"]["n_clipped"]) <= (~ok).sum()
+
+
+def test_gae_truncation():
+    P = _P()
+    E, T = 64, 200
+    rng = np.random.default_rng(4)
+    r, V = rng.normal(size=(E, T)).astype(np.float32), rng.normal(size=(E, T)).astype(np.float32)
+    B = rng.normal(size=(E, T)).astype(np.float32)
+    d = rng.choice([0, 1, 2], size=(E, T), p=[0.96, 0.02, 0.02]).astype(np.uint8)
+    lv = rng.normal(size=E).astype(np.float32)
+    buf = P.TrajectoryBuffer.allocate(E, T, 1)
+    buf.reward.copy_(_cuda(r))
+    buf.value.copy_(_cuda(V))
+    buf.done.copy_(_cuda(d))
+    buf.version.fill_(100)
+    buf.slot_key.fill_(1)
+    adv = torch.zeros(E, T, device="cuda")
+    ret = torch.zeros(E, T, device="cuda")
+    st = torch.zeros(24, dtype=torch.float64, device="cuda")
+    P.rlvla_advantages(buf, _cuda(lv), P.adv_params("gae", gamma=0.99, lam=0.95, n_env_global=E,
+                                                    cur_version=100, boot_value=_cuda(B)),
+                       adv, ret, st, P.workspace(E))
+    a, rr = O_adv.gae(r, V, d, np.ones((E, T)), lv, 0.99, 0.95, boot_value=B)
+    fl = max(1e-3, float(np.sqrt(np.mean(a ** 2))))
+    H.assert_close_rel(adv.cpu().numpy(), a, 1e-5, fl, "adv (truncation)")
+    H.assert_close_rel(ret.cpu().numpy(), rr, 1e-5, fl, "ret (truncation)")

@@ -20,7 +20,7 @@ def _gpu_advantages(case, mode, buf, whiten=False):
     E, T = case.n_env, cfg.t_steps
     dev = "cuda"
     ws = P.workspace(E, device=dev)
-    stats = torch.zeros(16, dtype=torch.float64, device=dev)
+    stats = torch.zeros(24, dtype=torch.float64, device=dev)
     adv = torch.zeros(E, T, dtype=torch.float32, device=dev)
     ret = torch.zeros(E, T, dtype=torch.float32, device=dev)
     lv = torch.from_numpy(case.traj.last_value[case.env_lo:case.env_hi]).to(dev)
@@ -48,7 +48,7 @@ def _gpu_loss(case, buf, adv, stats, ws, tok_den=0.0):
     fa = P.ppo_args(logp_behav=buf.logp_behav.view(-1), adv=adv.view(-1), version=buf.version.view(-1),
                     slot_key=buf.slot_key.view(-1), a_tok=A, cur_version=CUR, max_staleness=1,
                     tok_denominator=tok_den, adv_stats=stats, out_grad_logp=g, out_loss_tok=lt)
-    st2 = torch.zeros(16, dtype=torch.float64, device=dev)
+    st2 = torch.zeros(24, dtype=torch.float64, device=dev)
     P.rlvla_logprob_fwd_bwd(logits, buf.tokens.view(-1), logp=logp, lse=lse, fused=fa,
                             dlogits=dx, stats=st2, ws=ws)
     torch.cuda.synchronize()
@@ -132,7 +132,7 @@ def test_tiny_full_path_grpo():
         assert abs(st[slot] - rs[key]) <= 1e-5 * max(1.0, abs(rs[key])), key
     assert st[11] == rs["n_loss_tok"] and st[12] == rs["n_stale_tok"] and st[13] == rs["n_bad_tok"]
     assert abs(st[7] - rs["n_clipped"]) <= ref["near_tie"]
-    assert st[15] == oadv["counts"]["n_tok"]
+    assert st[18] == oadv["counts"]["n_tok"]
     # the fault injections really happened
     assert rs["n_stale_tok"] > 0 and rs["n_bad_tok"] == 0
 

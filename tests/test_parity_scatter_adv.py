@@ -76,7 +76,7 @@ def test_gae_matches_oracle(T, E, done_p, valid_p, whiten, gamma, lam):
     buf = _gpu_buffer(reward, value, done, valid, ver, tokens)
     adv = torch.zeros(E, T, device="cuda")
     ret = torch.zeros(E, T, device="cuda")
-    stats = torch.zeros(16, dtype=torch.float64, device="cuda")
+    stats = torch.zeros(24, dtype=torch.float64, device="cuda")
     prm = P.adv_params("gae", gamma=gamma, lam=lam, whiten=whiten, n_env_global=E,
                        cur_version=100, max_staleness=1)
     P.rlvla_advantages(buf, torch.from_numpy(lv).cuda(), prm, adv, ret, stats, P.workspace(E))
@@ -113,7 +113,7 @@ def test_grpo_matches_oracle(E, G, explicit, unbiased):
     gid = (np.arange(E) % (E // G)) if explicit else (np.arange(E) // G)
     adv = torch.zeros(E, T, device="cuda")
     ret = torch.zeros(E, T, device="cuda")
-    stats = torch.zeros(16, dtype=torch.float64, device="cuda")
+    stats = torch.zeros(24, dtype=torch.float64, device="cuda")
     prm = P.adv_params("grpo", group_id=torch.from_numpy(gid.astype(np.int32)).cuda() if explicit else None,
                        group_size=G, std_unbiased=unbiased, n_env_global=E, cur_version=100)
     P.rlvla_advantages(buf, None, prm, adv, ret, stats, P.workspace(E))
@@ -138,7 +138,7 @@ def test_advantages_deterministic():
     for _ in range(3):
         adv = torch.zeros(256, 512, device="cuda")
         ret = torch.zeros(256, 512, device="cuda")
-        st = torch.zeros(16, dtype=torch.float64, device="cuda")
+        st = torch.zeros(24, dtype=torch.float64, device="cuda")
         P.rlvla_advantages(buf, torch.from_numpy(lv).cuda(),
                            P.adv_params("gae", whiten=True, n_env_global=256, cur_version=100),
                            adv, ret, st, ws)

@@ -44,19 +44,19 @@ def test_streamer_equals_full_batch(cfg_name, n_env):
     R = x.shape[0]
     N = float(oadv["counts"]["n_tok"])
     ws = P.workspace(n_env)
-    st_full = torch.zeros(16, dtype=torch.float64, device="cuda")
+    st_full = torch.zeros(24, dtype=torch.float64, device="cuda")
     lf, gf, df = _fused(P, x, tgt, buf, adv, (0, R), A, N, st_full, ws, False)
     # uneven micro-batches of whole decision steps, in arrival order
     cuts = [0, 3 * A, 17 * A, (R // A // 2) * A, R]
-    st_mb = torch.zeros(16, dtype=torch.float64, device="cuda")
+    st_mb = torch.zeros(24, dtype=torch.float64, device="cuda")
     outs = [_fused(P, x, tgt, buf, adv, (a, b), A, N, st_mb, ws, True) for a, b in zip(cuts, cuts[1:])]
     torch.cuda.synchronize()
     assert torch.equal(torch.cat([o[0] for o in outs]), lf)
     assert torch.equal(torch.cat([o[1] for o in outs]), gf)
     assert torch.equal(torch.cat([o[2] for o in outs]), df)
     a, b = st_full.cpu().numpy(), st_mb.cpu().numpy()
-    np.testing.assert_allclose(b[6:15], a[6:15], rtol=1e-12, atol=1e-15)
-    assert b[15] == a[15] == N
+    np.testing.assert_allclose(b[6:18], a[6:18], rtol=1e-12, atol=1e-15)
+    assert b[18] == a[18] == N
     # and the accumulated stats equal the oracle's
     tv = O_path.token_view(obuf, oadv["adv"].astype(np.float32).astype(np.float64), A, synth.CUR_VERSION)
     tot = {}

@@ -70,7 +70,7 @@ def main():
     # GRPO with groups spanning ranks (C2 + C1)
     adv = torch.zeros(E_r, T, device=dev)
     ret = torch.zeros(E_r, T, device=dev)
-    st = torch.zeros(16, dtype=torch.float64, device=dev)
+    st = torch.zeros(24, dtype=torch.float64, device=dev)
     P.rlvla_advantages(buf, lv, P.adv_params("grpo", group_id=gid, group_size=4, env_offset=lo,
                                              n_env_global=E, cur_version=CUR), adv, ret, st, ws,
                        comm=comm)
@@ -86,7 +86,7 @@ def main():
     assert (s[0], s[3], s[4], s[5]) == tuple(tot.cpu().numpy().tolist()), (s[:6], tot)
     # GAE + global whitening (C1)
     adv2 = torch.zeros(E_r, T, device=dev)
-    st2 = torch.zeros(16, dtype=torch.float64, device=dev)
+    st2 = torch.zeros(24, dtype=torch.float64, device=dev)
     P.rlvla_advantages(buf, lv, P.adv_params("gae", whiten=True, env_offset=lo, n_env_global=E,
                                              cur_version=CUR), adv2, ret, st2, ws, comm=comm)
     a_gae, _ = O_adv.gae(obuf["reward"], obuf["value"], obuf["done"], valid, traj.last_value[lo:hi], 0.99, 0.95)
@@ -101,7 +101,7 @@ def main():
     logp = torch.empty(R, device=dev)
     g = torch.empty(R, device=dev)
     dx = torch.empty_like(xr)
-    st3 = torch.zeros(16, dtype=torch.float64, device=dev)
+    st3 = torch.zeros(24, dtype=torch.float64, device=dev)
     fa = P.ppo_args(logp_behav=buf.logp_behav.view(-1), adv=adv.view(-1), version=buf.version.view(-1),
                     slot_key=buf.slot_key.view(-1), a_tok=A, cur_version=CUR, adv_stats=st,
                     out_grad_logp=g)
@@ -119,7 +119,7 @@ def main():
     rs = rs.cpu().numpy()
     assert abs(s3[6] - rs[0]) <= 1e-5 * max(1e-3, abs(rs[0])), (s3[6], rs[0])
     assert s3[11] == rs[1] and abs(s3[9] - rs[2]) <= 1e-5 * abs(rs[2])
-    assert s3[15] == tot[1].item()
+    assert s3[18] == tot[1].item()
     dist.barrier()
     if rank == 0:
         print(f"MGPU PARITY OK world={world} nccl={P.rlvla_nccl_version()}", flush=True)

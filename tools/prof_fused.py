@@ -42,7 +42,7 @@ def main():
     adv = torch.randn(S, generator=g, device=dev)
     ver = torch.full((S,), 100, dtype=torch.int32, device=dev)
     key = torch.ones(S, dtype=torch.int64, device=dev)
-    stats = torch.zeros(16, dtype=torch.float64, device=dev)
+    stats = torch.zeros(24, dtype=torch.float64, device=dev)
     ws = P.workspace(1)
     fa = P.ppo_args(logp_behav=lb, adv=adv, version=ver, slot_key=key, a_tok=A, cur_version=100,
                     tok_denominator=float(R))

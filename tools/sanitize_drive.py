@@ -24,7 +24,7 @@ def main():
         buf2, _ = H.gpu_scatter(case, chunk=5000)           # multi-CTA claim/write kernels
         E, T, A = case.n_env, cfg.t_steps, cfg.a_tok
         ws = P.workspace(E)
-        stats = torch.zeros(16, dtype=torch.float64, device="cuda")
+        stats = torch.zeros(24, dtype=torch.float64, device="cuda")
         adv = torch.zeros(E, T, device="cuda")
         ret = torch.zeros(E, T, device="cuda")
         lv = torch.from_numpy(case.traj.last_value).cuda()
@@ -40,7 +40,7 @@ def main():
         lse = torch.empty(R, device="cuda")
         g = torch.empty(R, device="cuda")
         dx = torch.empty_like(x)
-        st = torch.zeros(16, dtype=torch.float64, device="cuda")
+        st = torch.zeros(24, dtype=torch.float64, device="cuda")
         P.rlvla_logprob_fwd_bwd(x, tgt, logp=logp, lse=lse, stats=st, ws=ws)
         for prox in (None, buf.logp_behav.view(-1)):
             fa = P.ppo_args(logp_behav=buf.logp_behav.view(-1), logp_prox=prox, adv=adv.view(-1),
