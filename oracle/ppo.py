@@ -136,8 +136,8 @@ def ppo_loss_chunk(logp, logp_behav, adv_step, mask_tok, step_of_tok, n_steps_to
 def value_loss(v_new, v_old, ret, mask, *, clip_eps=0.2, n_den=None):
     """Clipped value loss per decision step (PPO value head, NEXT-2; paper-silent, reading
     R22): L = 0.5 max((v - R)^2, (v_old + clip(v - v_old, -e, e) - R)^2); e <= 0 => plain
-    0.5 (v - R)^2. Loss = sum m L / N; dLoss/dv from the larger branch (ties: unclipped),
-    the clipped branch passing gradient only inside the clip interval."""
+    0.5 (v - R)^2. Loss = sum m L / N; dLoss/dv from the larger branch; the clipped branch
+    counts only where the clip moved v (|v - v_old| > e), and there d clip/dv = 0."""
     v = np.asarray(v_new, np.float64)
     vo = np.asarray(v_old, np.float64)
     R = np.asarray(ret, np.float64)
@@ -149,8 +149,10 @@ def value_loss(v_new, v_old, ret, mask, *, clip_eps=0.2, n_den=None):
         d = v - vo
         vc = vo + np.clip(d, -clip_eps, clip_eps)
         c = (vc - R) ** 2
-        use_c = c > u
-        g = np.where(use_c, (vc - R) * (np.abs(d) < clip_eps), v - R)
+        # the clipped branch counts only where the clip moved v (|d| > e); inside the
+        # interval v_clip == v and both branches agree (reading R22)
+        use_c = (np.abs(d) > clip_eps) & (c > u)
+        g = np.where(use_c, 0.0, v - R)
         L = 0.5 * np.maximum(u, c)
     else:
         use_c = np.zeros_like(m)

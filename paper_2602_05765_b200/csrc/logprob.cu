@@ -163,6 +163,28 @@ __device__ __forceinline__ double resolve_pc(const Lp& p, PpoConst& pc) {
   return N;
 }
 
+// ln S and logp = (x_a - M) - ln S without cancellation when the target carries most of
+// the mass: S = e_a (1 + S_rest/e_a), so logp = -log1p(S_rest/e_a) and
+// ln S = t_a ln2 + log1p(S_rest/e_a) (a saturated row keeps logp ~ -1e-24 instead of 0).
+// e_a below 2^-100 (target far from the max) falls back to the direct form.
+struct LseParts {
+  float lnS;
+  float logp;
+};
+__device__ __forceinline__ LseParts lse_parts(float xa, float M, float ta, float ea, float Srest,
+                                              float Stot, bool tgt_ok) {
+  LseParts o;
+  if (tgt_ok && ea > 7.9e-31f) {
+    const float l1 = log1pf(Srest / ea);
+    o.logp = -l1;
+    o.lnS = fmaf(ta, kLn2, l1);
+  } else {
+    o.lnS = __logf(Stot);
+    o.logp = (xa - M) - o.lnS;
+  }
+  return o;
+}
+
 // dx at the target column: g (1 - p_a) + c p_a (log p_a + H), with 1 - p_a = S_rest / S
 __device__ __forceinline__ float target_grad(const RowGrad& rg, float Srest, float ea, float invS,
                                              float logp, float H) {
@@ -436,9 +458,10 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
         const float ta = (xa - M) * L2E;
         const float ea = tgt_ok ? ex2(ta) : 0.f;
         const float Stot = Srest + ea;
-        const float lnS = __logf(Stot);
+        const LseParts lp = lse_parts(xa, M, ta, ea, Srest, Stot, tgt_ok);
+        const float lnS = lp.lnS;
         const float lse_row = M + lnS;
-        const float logp = (xa - M) - lnS;
+        const float logp = lp.logp;
         const float invS = __fdividef(1.f, Stot);
         const float Ctot = Csum + (tgt_ok ? ea * fmaxf(ta, -256.f) : 0.f);
         const float H = lnS - Ctot * invS * kLn2;
@@ -595,9 +618,10 @@ __global__ void __launch_bounds__(256) lp_warp_kernel(Lp p) {
       const float ta = (xa - Ms) * L2E;
       ea = tgt_ok ? ex2(ta) : 0.f;
       Stot = Srest + ea;
-      lnS = __logf(Stot);
+      const LseParts lp = lse_parts(xa, M, ta, ea, Srest, Stot, tgt_ok);
+      lnS = lp.lnS;
       const float lse_row = M + lnS;
-      logp = (xa - M) - lnS;
+      logp = lp.logp;
       H = lnS - (Cs + (tgt_ok ? ea * fmaxf(ta, -256.f) : 0.f)) / (L2E * Stot);
       const RowMeta rm = load_meta<MODE>(p, r);
       rg = finish_row<MODE>(p, pc, r, a, lse_row, logp, H, rm, lane == 0,
@@ -712,9 +736,10 @@ __global__ void __launch_bounds__(256) lp_generic_kernel(Lp p) {
       const float ta = (xa - Ms) * L2E;
       ea = tgt_ok ? ex2(ta) : 0.f;
       Stot = Srest + ea;
-      lnS = __logf(Stot);
+      const LseParts lp = lse_parts(xa, M, ta, ea, Srest, Stot, tgt_ok);
+      lnS = lp.lnS;
       lse_row = M + lnS;
-      logp = (xa - M) - lnS;
+      logp = lp.logp;
       H = lnS - (Cs + (tgt_ok ? ea * fmaxf(ta, -256.f) : 0.f)) / (L2E * Stot);
       const RowMeta rm = load_meta<MODE>(p, r);
       rg = finish_row<MODE>(p, pc, r, a, lse_row, logp, H, rm, tid == 0, want_stats ? sacc : nullptr);

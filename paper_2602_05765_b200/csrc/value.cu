@@ -32,8 +32,10 @@ __global__ void __launch_bounds__(256) value_loss_kernel(ValueArgs a) {
         const float vc = a.v_old[s] + fminf(fmaxf(d, -a.clip_eps), a.clip_eps);
         const float dc = vc - R;
         const float c = dc * dc;
-        use_c = c > u;  // ties: unclipped branch
-        g = use_c ? (fabsf(d) < a.clip_eps ? dc : 0.f) : du;
+        // the clipped branch counts only where the clip moved v (inside the interval
+        // v_clip == v, so c vs u would be a rounding coin-flip with the same gradient)
+        use_c = fabsf(d) > a.clip_eps && c > u;
+        g = use_c ? 0.f : du;  // outside the interval d clip / dv = 0
         L = 0.5f * fmaxf(u, c);
       } else {
         g = du;

@@ -29,12 +29,23 @@ def bf16_rne_bits(x64: np.ndarray) -> np.ndarray:
     return t.to(torch.bfloat16).view(torch.int16).numpy().astype(np.int32) & 0xFFFF
 
 
-def assert_bf16_ulp(gpu_bits: np.ndarray, ref64: np.ndarray, max_ulp: int = 1, ftz=1.2e-38):
-    """|ord(gpu) - ord(RNE_bf16(ref))| <= max_ulp, ±0 equal; refs below FLT_MIN may flush."""
+def bf16_value(bits: np.ndarray) -> np.ndarray:
+    b = torch.from_numpy((np.asarray(bits).astype(np.int32) & 0xFFFF).astype(np.uint16).view(np.int16))
+    return b.view(torch.bfloat16).to(torch.float64).numpy()
+
+
+def assert_bf16_ulp(gpu_bits: np.ndarray, ref64: np.ndarray, max_ulp: int = 1, ftz=1.2e-38,
+                    abs_floor=None):
+    """|ord(gpu) - ord(RNE_bf16(ref))| <= max_ulp, ±0 equal; refs below FLT_MIN may flush.
+    `abs_floor` (array or scalar): an element also passes when |gpu - ref| <= abs_floor —
+    for values that are a cancelling sum, whose fp32 error bound is relative to the sum of
+    the terms' magnitudes rather than to the value."""
     rb = bf16_rne_bits(ref64)
     d = np.abs(bf16_ord(gpu_bits) - bf16_ord(rb))
     tiny = np.abs(ref64) < ftz
     bad = (d > max_ulp) & ~tiny
+    if abs_floor is not None and bad.any():
+        bad &= ~(np.abs(bf16_value(gpu_bits) - ref64) <= abs_floor)
     if bad.any():
         i = np.argwhere(bad)[0]
         raise AssertionError(f"{int(bad.sum())} bf16 elements off by > {max_ulp} ulp; first at "
