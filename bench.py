@@ -312,7 +312,7 @@ def run_ours(args):
     # ---- e2e: records from pinned host memory, stats back to host, every step -------
     e2e_ms = None
     if not args.no_e2e:
-        st_pinned = torch.empty(16, dtype=torch.float64).pin_memory()
+        st_pinned = torch.empty(lstats.numel(), dtype=torch.float64).pin_memory()
         dst = {k: getattr(drec, k) for k in host}
 
         def e2e_step():
@@ -378,7 +378,7 @@ def run_ours(args):
         "clocks": clocks,
         "e2e": None if e2e_ms is None else {
             "value": units_per_step * args.steps / (e2e_ms / 1e3), "unit": UNIT,
-            "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": 128,
+            "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(st_pinned.numel() * 8),
             "note": "step records H2D from pinned memory + loss stats D2H inside the timed "
                     "region; logits are the VLA forward output produced on the device"},
         "gpu_launches": launches_per_step * args.steps,

@@ -104,6 +104,8 @@ def lib() -> ctypes.CDLL:
                 "(there is no CPU fallback)")
         L = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
+            if os.environ.get("RLVLA_LIB") and not hasattr(L, name):
+                continue  # an older revision under A/B timing (tools/ab_variants.py)
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

@@ -50,64 +50,94 @@ struct PpoConst {
   float invN;
 };
 
-// Returns g = dLoss/dlogp for the row; fills rs and *loss_tok (m * (L_pg + kl k3_ref)).
-__device__ __forceinline__ float ppo_row(const PpoConst& c, const PpoRowIn& in, RowStats& rs,
-                                         float* loss_tok) {
+// Intermediate values of one row: ppo_grad computes what the gradient needs (the only
+// part on the fused kernel's critical path), ppo_stats the rest once g is published.
+struct PpoMid {
+  bool m, base, clipped, dual;
+  int lag;
+  float lr, rho, w, J, lq;
+};
+
+// g = dLoss/dlogp for the row (including 1/N)
+__device__ __forceinline__ float ppo_grad(const PpoConst& c, const PpoRowIn& in, PpoMid& t) {
   const bool usable = in.tgt_status == 0;
-  const int lag = c.cur_version - in.ver;
-  const bool base = in.valid && usable;
-  const bool m = base && lag >= 0 && lag <= c.eta;
-  rs.stale = (base && lag > c.eta) ? 1.f : 0.f;
-  rs.bad = ((in.valid && (in.tgt_status == 2 || in.tgt_status == 3)) || (base && lag < 0)) ? 1.f : 0.f;
-  float g = 0.f, L = 0.f;
+  t.lag = c.cur_version - in.ver;
+  t.base = in.valid && usable;
+  t.m = t.base && t.lag >= 0 && t.lag <= c.eta;
+  t.clipped = t.dual = false;
+  t.lr = t.rho = t.J = t.lq = 0.f;
+  t.w = 1.f;
+  if (!t.m) return 0.f;
+  if (c.has_prox) {
+    t.lr = in.logp - in.lpp;
+  } else {
+    t.lr = in.logp - in.lpb;
+  }
+  // (measured and rejected: rho = p_a e^{-lp_base} with e^{-lp_base} precomputed before the
+  // row's sums — slower, and rho = 1 is no longer exact when logp == logp_behav)
+  t.rho = __expf(t.lr);
+  if (c.has_prox) {
+    t.w = __expf(in.lpp - in.lpb);
+    if (c.is_cap > 0.f) t.w = fminf(t.w, c.is_cap);
+  }
+  const float A = in.adv;
+  const float rc = fminf(fmaxf(t.rho, c.lo), c.hi);
+  t.J = fminf(t.rho * A, rc * A);
+  t.clipped = (A > 0.f && t.rho > c.hi) || (A < 0.f && t.rho < c.lo);
+  // dual clip (c > 1): for A < 0 the objective is max(J, c A); strict > (tie: J branch)
+  t.dual = c.dual_clip > 1.f && A < 0.f && c.dual_clip * A > t.J;
+  if (t.dual) t.J = c.dual_clip * A;
+  float gr = (t.clipped || t.dual) ? 0.f : -t.w * A * t.rho;
+  if (c.has_ref) {
+    // k3 = e^{q} - q - 1 with q = logp_ref - logp; dk3/dlogp = 1 - e^{q}
+    t.lq = in.lref - in.logp;
+    gr += c.kl_coef * (-expm1f(t.lq));
+  }
+  return gr * c.invN;
+}
+
+// k3-type divergence e^x - 1 - x, cancellation-free near x = 0 (Taylor to x^6)
+__device__ __forceinline__ float k3_of(float x, float ex) {
+  return fabsf(x) < 0.125f
+             ? x * x * (0.5f + x * (1.f / 6.f + x * (1.f / 24.f + x * (1.f / 120.f + x * (1.f / 720.f)))))
+             : (ex - 1.f - x);
+}
+
+// statistics and the per-token loss m (L_pg + kl k3_ref) from ppo_grad's intermediates
+__device__ __forceinline__ void ppo_stats(const PpoConst& c, const PpoRowIn& in, const PpoMid& t,
+                                          RowStats& rs, float* loss_tok) {
+  rs.stale = (t.base && t.lag > c.eta) ? 1.f : 0.f;
+  rs.bad = ((in.valid && (in.tgt_status == 2 || in.tgt_status == 3)) || (t.base && t.lag < 0)) ? 1.f : 0.f;
   rs.loss = rs.clipped = rs.k3 = rs.ent = rs.rho = rs.m = rs.logp = 0.f;
   rs.kl_ref = rs.dual = rs.pg = 0.f;
-  if (m) {
-    float lr, w;
-    if (c.has_prox) {
-      w = __expf(in.lpp - in.lpb);
-      if (c.is_cap > 0.f) w = fminf(w, c.is_cap);
-      lr = in.logp - in.lpp;
-    } else {
-      w = 1.f;
-      lr = in.logp - in.lpb;
-    }
-    const float rho = __expf(lr);
-    const float A = in.adv;
-    const float rc = fminf(fmaxf(rho, c.lo), c.hi);
-    float J = fminf(rho * A, rc * A);
-    const bool clipped = (A > 0.f && rho > c.hi) || (A < 0.f && rho < c.lo);
-    // dual clip (c > 1): for A < 0 the objective is max(J, c A); strict > (tie: J branch)
-    const bool dual = c.dual_clip > 1.f && A < 0.f && c.dual_clip * A > J;
-    if (dual) J = c.dual_clip * A;
-    const float Lpg = -w * J;
-    float gr = (clipped || dual) ? 0.f : -w * A * rho;
+  float L = 0.f;
+  if (t.m) {
+    const float Lpg = -t.w * t.J;
     L = Lpg;
     if (c.has_ref) {
-      // k3 = e^{lr} - lr - 1 with lr = logp_ref - logp; dk3/dlogp = 1 - e^{lr}
-      const float lq = in.lref - in.logp;
-      const float k3r = fabsf(lq) < 0.125f
-                            ? lq * lq * (0.5f + lq * (1.f / 6.f + lq * (1.f / 24.f + lq * (1.f / 120.f + lq * (1.f / 720.f)))))
-                            : (__expf(lq) - 1.f - lq);
+      const float k3r = k3_of(t.lq, __expf(t.lq));
       L += c.kl_coef * k3r;
-      gr += c.kl_coef * (-expm1f(lq));
       rs.kl_ref = k3r;
     }
-    g = gr * c.invN;
     rs.loss = L;
     rs.pg = Lpg;
-    rs.clipped = clipped ? 1.f : 0.f;
-    rs.dual = dual ? 1.f : 0.f;
-    // k3 = rho - 1 - ln rho = expm1(lr) - lr, cancellation-free near rho = 1 (Taylor to lr^6)
-    rs.k3 = fabsf(lr) < 0.125f
-                ? lr * lr * (0.5f + lr * (1.f / 6.f + lr * (1.f / 24.f + lr * (1.f / 120.f + lr * (1.f / 720.f)))))
-                : (rho - 1.f - lr);
+    rs.clipped = t.clipped ? 1.f : 0.f;
+    rs.dual = t.dual ? 1.f : 0.f;
+    rs.k3 = k3_of(t.lr, t.rho);  // rho - 1 - ln rho
     rs.ent = in.H;
-    rs.rho = rho;
+    rs.rho = t.rho;
     rs.m = 1.f;
     rs.logp = in.logp;
   }
   *loss_tok = L;
+}
+
+// Returns g = dLoss/dlogp for the row; fills rs and *loss_tok (m * (L_pg + kl k3_ref)).
+__device__ __forceinline__ float ppo_row(const PpoConst& c, const PpoRowIn& in, RowStats& rs,
+                                         float* loss_tok) {
+  PpoMid t;
+  const float g = ppo_grad(c, in, t);
+  ppo_stats(c, in, t, rs, loss_tok);
   return g;
 }
 

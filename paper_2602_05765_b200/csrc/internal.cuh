@@ -38,9 +38,17 @@ inline Workspace carve(void* ws) {
 // ------------------------------------------------------------------------------------
 // device helpers
 // ------------------------------------------------------------------------------------
+// warp max in one instruction (sm_100a redux.sync .f32 -> CREDUX.MAX.F32); without .NaN
+// a NaN input is ignored like fmaxf's
 __device__ __forceinline__ float warp_max(float v) {
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+// sum over lanes 0..15 (xor tree within each half-warp: the result is valid in lanes 0..15)
+__device__ __forceinline__ float half_warp_sum(float v) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 __device__ __forceinline__ float warp_sum(float v) {

@@ -97,41 +97,84 @@ struct RowGrad {
   float c;
 };
 
-// `writer` stores the per-row outputs and accumulates the statistics
+#ifndef RLVLA_SPLIT_STATS
+#define RLVLA_SPLIT_STATS 1  // 0: statistics evaluated before pass C's scalars are published
+#endif
+
+// per-row results kept until they are stored (after pass C's scalars are published)
+struct RowOut {
+  float logp, lse;
+  PpoRowIn in;
+  PpoMid mid;
+#if !RLVLA_SPLIT_STATS
+  RowStats rs;
+  float lt;
+#endif
+};
+
+// critical part: the row's g and c (and what the statistics need later)
+template <int MODE>
+__device__ __forceinline__ RowGrad eval_row(const Lp& p, const PpoConst& pc, int a, float lse,
+                                            float logp, float H, const RowMeta& mt, RowOut& o) {
+  const int st = row_status(a, p.V, lse, logp);
+  RowGrad out{0.f, 0.f};
+  o.lse = lse;
+  o.in.tgt_status = st;
+  o.in.logp = (st == 1 || st == 2) ? 0.f : logp;
+  o.in.H = H;
+  o.logp = o.in.logp;
+  if (MODE == MODE_FUSED) {
+    o.in.lpb = mt.lpb;
+    o.in.lpp = mt.lpp;
+    o.in.lref = mt.lref;
+    o.in.adv = mt.adv;
+    o.in.ver = mt.ver;
+    o.in.valid = mt.key != 0ull;
+    out.g = ppo_grad(pc, o.in, o.mid);
+    out.c = o.mid.m ? pc.ent_coef * pc.invN : 0.f;
+#if !RLVLA_SPLIT_STATS
+    ppo_stats(pc, o.in, o.mid, o.rs, &o.lt);
+#endif
+  }
+#if !RLVLA_SPLIT_STATS
+  else {
+    fwd_row_stats(o.in, o.rs);
+    o.lt = 0.f;
+  }
+#endif
+  return out;
+}
+
+// per-row outputs and statistics (one writer thread per row)
+template <int MODE>
+__device__ __forceinline__ void write_row(const Lp& p, const PpoConst& pc, int64_t r,
+                                          const RowGrad& rg, const RowOut& o, double* acc) {
+#if RLVLA_SPLIT_STATS
+  RowStats rs;
+  float lt = 0.f;
+  if (MODE == MODE_FUSED) ppo_stats(pc, o.in, o.mid, rs, &lt);
+  else fwd_row_stats(o.in, rs);
+#else
+  const RowStats& rs = o.rs;
+  const float lt = o.lt;
+#endif
+  p.logp[r] = o.logp;
+  if (p.lse_out) p.lse_out[r] = o.lse;
+  if (MODE == MODE_FUSED) {
+    if (p.out_g) p.out_g[r] = rg.g;
+    if (p.out_L) p.out_L[r] = lt;
+  }
+  if (acc) acc_stats(acc, rs);
+}
+
 template <int MODE>
 __device__ __forceinline__ RowGrad finish_row(const Lp& p, const PpoConst& pc, int64_t r, int a,
                                               float lse, float logp, float H, const RowMeta& mt,
                                               bool writer, double* acc) {
-  const int st = row_status(a, p.V, lse, logp);
-  RowGrad out{0.f, 0.f};
-  float lt = 0.f;
-  RowStats rs;
-  PpoRowIn in;
-  in.tgt_status = st;
-  in.logp = (st == 1 || st == 2) ? 0.f : logp;
-  in.H = H;
-  if (MODE == MODE_FUSED) {
-    in.lpb = mt.lpb;
-    in.lpp = mt.lpp;
-    in.lref = mt.lref;
-    in.adv = mt.adv;
-    in.ver = mt.ver;
-    in.valid = mt.key != 0ull;
-    out.g = ppo_row(pc, in, rs, &lt);
-    out.c = rs.m != 0.f ? pc.ent_coef * pc.invN : 0.f;
-  } else {
-    fwd_row_stats(in, rs);
-  }
-  if (writer) {
-    p.logp[r] = in.logp;
-    if (p.lse_out) p.lse_out[r] = lse;
-    if (MODE == MODE_FUSED) {
-      if (p.out_g) p.out_g[r] = out.g;
-      if (p.out_L) p.out_L[r] = lt;
-    }
-    if (acc) acc_stats(acc, rs);
-  }
-  return out;
+  RowOut o;
+  const RowGrad rg = eval_row<MODE>(p, pc, a, lse, logp, H, mt, o);
+  if (writer) write_row<MODE>(p, pc, r, rg, o, acc);
+  return rg;
 }
 
 template <int MODE>
@@ -163,10 +206,15 @@ __device__ __forceinline__ double resolve_pc(const Lp& p, PpoConst& pc) {
   return N;
 }
 
-// ln S and logp = (x_a - M) - ln S without cancellation when the target carries most of
-// the mass: S = e_a (1 + S_rest/e_a), so logp = -log1p(S_rest/e_a) and
-// ln S = t_a ln2 + log1p(S_rest/e_a) (a saturated row keeps logp ~ -1e-24 instead of 0).
-// e_a below 2^-100 (target far from the max) falls back to the direct form.
+// ln S and logp = (x_a - M) - ln S. The direct form has an absolute error of a few fp32
+// ulps of ln S, which is all any consumer needs (the ratio e^{logp - logp_behav} and every
+// gradient term carry it as a relative error). The log1p form keeps relative accuracy for
+// |logp| << 1 (a saturated row: logp ~ -1e-24 instead of 0): S = e_a (1 + S_rest/e_a), so
+// logp = -log1p(S_rest/e_a) and ln S = t_a ln2 + log1p(S_rest/e_a). A/B (tools/ab_variants.py):
+// the branch costs 0.7% of the fused kernel's time, so the product keeps the direct form.
+#ifndef RLVLA_LSE_MODE
+#define RLVLA_LSE_MODE 0  // 0: direct form; 1: log1p form whenever e_a > 2^-100; 2: when S_rest < e_a
+#endif
 struct LseParts {
   float lnS;
   float logp;
@@ -174,8 +222,15 @@ struct LseParts {
 __device__ __forceinline__ LseParts lse_parts(float xa, float M, float ta, float ea, float Srest,
                                               float Stot, bool tgt_ok) {
   LseParts o;
-  if (tgt_ok && ea > 7.9e-31f) {
-    const float l1 = log1pf(Srest / ea);
+#if RLVLA_LSE_MODE == 0
+  const bool use = false;
+#elif RLVLA_LSE_MODE == 1
+  const bool use = tgt_ok && ea > 7.9e-31f;
+#else
+  const bool use = tgt_ok && Srest < ea;
+#endif
+  if (use) {
+    const float l1 = log1pf(__fdividef(Srest, ea));
     o.logp = -l1;
     o.lnS = fmaf(ta, kLn2, l1);
   } else {
@@ -224,6 +279,15 @@ struct __align__(16) StageMeta {
   float lref;
   float pad;
 };
+
+__device__ __forceinline__ void read_meta(const Lp& p, const StageMeta* mt, RowMeta& rm) {
+  rm.lpb = mt->lpb;
+  if (p.lpp) rm.lpp = mt->lpp;
+  if (p.lref) rm.lref = mt->lref;
+  rm.adv = mt->adv;
+  rm.ver = mt->ver;
+  rm.key = mt->key;
+}
 
 __device__ __forceinline__ int ld_volatile_s32(const int32_t* p) {
   return *reinterpret_cast<const volatile int32_t*>(p);
@@ -280,7 +344,10 @@ __device__ __forceinline__ void scalars_sync(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(g + 3), "n"(kGroupThreads) : "memory");
 }
 
-template <int MODE>
+// XP: pass C from x (external bwd, or fused with the entropy bonus); otherwise from the e
+// values pass B kept in the stage. A template parameter so the common fused loop carries
+// no code of the other.
+template <int MODE, bool XP>
 __global__ void __launch_bounds__(kCtaThreads, 1)
     lp_tma_kernel(Lp p, int nstages, uint32_t stage_bytes) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -305,8 +372,9 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
   const double Nden = resolve_pc<MODE>(p, pc);
   // pass C runs in external-bwd mode and in fused mode with dlogits; it reuses the e
   // values of pass B (stored as bf16 in the stage) unless the entropy bonus needs x
+  constexpr bool kXPath = XP || MODE == MODE_BWD;
   const bool has_c = MODE == MODE_BWD || (MODE == MODE_FUSED && p.dx != nullptr);
-  const bool keep_e = MODE == MODE_FUSED && p.dx != nullptr && pc.ent_coef == 0.f;
+  const bool keep_e = MODE == MODE_FUSED && !kXPath && p.dx != nullptr;
   const float L2E = kLog2e;
 
   if (tid == 0) {
@@ -431,16 +499,10 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
       et = warp_sum(et);
       if (lane == 0) gred[gw] = make_float4(mw, s, et, 0.f);
       if (keep_e) fence_proxy_async();  // generic smem writes before the stage's next TMA fill
-      // warp 0 needs the row metadata; read it before the stage can be refilled
+      // warp 0 needs the row metadata: read before #1 only when the stage is refilled right
+      // after it (no pass C); otherwise after #1, so warp 0 reaches the barrier sooner
       RowMeta rm;
-      if (gw == 0 && MODE == MODE_FUSED) {
-        rm.lpb = mt->lpb;
-        if (p.lpp) rm.lpp = mt->lpp;
-        if (p.lref) rm.lref = mt->lref;
-        rm.adv = mt->adv;
-        rm.ver = mt->ver;
-        rm.key = mt->key;
-      }
+      if (gw == 0 && MODE == MODE_FUSED && !has_c) read_meta(p, mt, rm);
       group_sync(grp);  // #1: warp partials + x_a visible; stage no longer read in FWD mode
       if (!has_c && gt == 0 && k + nstages < nrow) {
         fence_proxy_async();
@@ -448,13 +510,15 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
       }
       if (gw == 0) {
         // ---- combine 16 warp partials, per-row epilogue (one warp) ------------------
+        if (MODE == MODE_FUSED && has_c) read_meta(p, mt, rm);
         const float xa = tgt_ok ? *gxa : 0.f;
         const float4 q = lane < kGroupWarps ? gred[lane] : make_float4(-INFINITY, 0.f, 0.f, 0.f);
         const float M = warp_max(q.x);
         const float sc = lane < kGroupWarps ? ex2((q.x - M) * L2E) : 0.f;
         const float mq = (q.x == -INFINITY) ? 0.f : q.x;
-        const float Srest = warp_sum(q.y * sc);
-        const float Csum = warp_sum(lane < kGroupWarps ? sc * (q.z + (mq - M) * L2E * q.y) : 0.f);
+        // the 16 warp partials sit in lanes 0..15; lane 0 (the only writer) gets the sums
+        const float Srest = half_warp_sum(q.y * sc);
+        const float Csum = half_warp_sum(lane < kGroupWarps ? sc * (q.z + (mq - M) * L2E * q.y) : 0.f);
         const float ta = (xa - M) * L2E;
         const float ea = tgt_ok ? ex2(ta) : 0.f;
         const float Stot = Srest + ea;
@@ -465,8 +529,8 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
         const float invS = __fdividef(1.f, Stot);
         const float Ctot = Csum + (tgt_ok ? ea * fmaxf(ta, -256.f) : 0.f);
         const float H = lnS - Ctot * invS * kLn2;
-        const RowGrad rg = finish_row<MODE>(p, pc, r, a, lse_row, logp, H, rm, lane == 0,
-                                            want_stats ? gacc + grp * 16 : nullptr);
+        RowOut ro;
+        const RowGrad rg = eval_row<MODE>(p, pc, a, lse_row, logp, H, rm, ro);
         if (has_c) {
           if (lane == 0) {
             RowScalars sc4;
@@ -480,6 +544,8 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
           __syncwarp();
           scalars_arrive(grp);  // #2 (producer side): the other warps may start pass C now
         }
+        // per-row outputs and statistics, off the pass-C critical path
+        if (lane == 0) write_row<MODE>(p, pc, r, rg, ro, want_stats ? gacc + grp * 16 : nullptr);
       } else if (has_c) {
         scalars_sync(grp);  // #2 (consumer side): row scalars published
       }
@@ -501,7 +567,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     // ---- pass C: dlogits (masked / clipped rows get exact zeros) ---------------------
     {
       __nv_bfloat16* drow = static_cast<__nv_bfloat16*>(p.dx) + int64_t(r) * p.ld;
-      const float kw = keep_e ? rsv.k1 * ex2((mws - rsv.M) * L2E) : rsv.k1;
+      const float kw = !kXPath ? rsv.k1 * ex2((mws - rsv.M) * L2E) : rsv.k1;
       const float nML = -rsv.M * L2E;
 #pragma unroll
       for (int i = 0; i < kVecPerThread; ++i) {
@@ -512,7 +578,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
             const uint4 w = rv[idx];
             const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
             uint32_t* ow = &o.x;
-            if (keep_e) {
+            if (!kXPath) {
               // FUSED: dx = g' 2^{(m_w - M) log2e} e, e from pass B (bf16 in SMEM)
 #pragma unroll
               for (int q = 0; q < 4; ++q) ow[q] = pack_bf16x2(kw * bf_lo(w4[q]), kw * bf_hi(w4[q]));
@@ -831,19 +897,22 @@ cudaError_t launch_mode(const LpArgs& a, Lp p, cudaStream_t s) {
     if (nst < 2) return cudaErrorInvalidConfiguration;
     const size_t smem = size_t(nst) * stage_bytes + fixed;
     // dynamic smem limit = opt-in max minus the kernel's static smem
-    static int attr_dyn[3] = {0, 0, 0};
-    if (attr_dyn[MODE] < int(smem)) {
+    const bool xp = MODE == MODE_FUSED && a.f.ent_coef != 0.f && a.dlogits != nullptr;
+    const void* fn = xp ? reinterpret_cast<const void*>(lp_tma_kernel<MODE, true>)
+                        : reinterpret_cast<const void*>(lp_tma_kernel<MODE, false>);
+    static int attr_dyn[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+    if (attr_dyn[MODE][xp] < int(smem)) {
       cudaFuncAttributes fa{};
-      cudaError_t e = cudaFuncGetAttributes(&fa, lp_tma_kernel<MODE>);
+      cudaError_t e = cudaFuncGetAttributes(&fa, fn);
       if (e != cudaSuccess) return e;
       if (smem + fa.sharedSizeBytes > size_t(device_info().smem_optin)) return cudaErrorInvalidConfiguration;
-      e = cudaFuncSetAttribute(lp_tma_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem));
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
-      attr_dyn[MODE] = int(smem);
+      attr_dyn[MODE][xp] = int(smem);
     }
     int grid = int(R < sms ? R : sms);
-    lp_tma_kernel<MODE><<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);
+    if (xp) lp_tma_kernel<MODE, true><<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);
+    else lp_tma_kernel<MODE, false><<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);
     return cudaGetLastError();
   }
   if (path == LP_PATH_WARP) {

@@ -12,8 +12,43 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
-    "element_clamp": ("RLVLA_PACKED_CLAMP=0",),
+    "lse_log1p_branch": ("RLVLA_LSE_MODE=2",),
+    "stats_first": ("RLVLA_SPLIT_STATS=0",),
 }
+# name -> git revision whose csrc/ + include/ are built as one more variant
+# (the ABI only grew at the end of its structs, so today's binding drives older libraries)
+REVISIONS = {"pre_next2": "6cd809f"}
+
+
+def build_revision(name, rev):
+    """Compile `rev`'s csrc with its own include/ into variants/<name>.so (scratch under build/)."""
+    from paper_2602_05765_b200 import build as B
+    src = os.path.join(B.BUILD, "rev_" + name)
+    for sub in ("paper_2602_05765_b200/csrc", "include"):
+        os.makedirs(os.path.join(src, sub), exist_ok=True)
+        files = subprocess.run(["git", "-C", ROOT, "ls-tree", "--name-only", f"{rev}:{sub}"],
+                               capture_output=True, text=True, check=True).stdout.split()
+        for f in files:
+            blob = subprocess.run(["git", "-C", ROOT, "show", f"{rev}:{sub}/{f}"],
+                                  capture_output=True, check=True).stdout
+            with open(os.path.join(src, sub, f), "wb") as fh:
+                fh.write(blob)
+    flags = [f if f != os.path.join(ROOT, "include") else os.path.join(src, "include")
+             for f in B._flags()]
+    objs = []
+    for cu in sorted(os.listdir(os.path.join(src, "paper_2602_05765_b200/csrc"))):
+        if not cu.endswith(".cu"):
+            continue
+        obj = os.path.join(src, cu + ".o")
+        subprocess.run([B.NVCC, "-c", os.path.join(src, "paper_2602_05765_b200/csrc", cu), "-o", obj]
+                       + flags, check=True, capture_output=True)
+        objs.append(obj)
+    nd = B.nccl_dir()
+    out = os.path.join(VAR, f"{name}.so")
+    subprocess.run([B.NVCC, "-shared", "-o", out] + objs + B.ARCH +
+                   ["-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
+                    "-Xlinker", "-rpath", "-Xlinker", os.path.join(nd, "lib")], check=True)
+    print(out)
 
 
 def build():
@@ -21,12 +56,14 @@ def build():
     os.makedirs(VAR, exist_ok=True)
     for name, defs in VARIANTS.items():
         print(B.build(out=os.path.join(VAR, f"{name}.so"), defines=defs))
+    for name, rev in REVISIONS.items():
+        build_revision(name, rev)
 
 
 def run(mode="fused", rounds=3):
     res = {}
     for _ in range(rounds):
-        for name in VARIANTS:
+        for name in list(VARIANTS) + list(REVISIONS):
             env = dict(os.environ, RLVLA_LIB=os.path.join(VAR, f"{name}.so"))
             out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "prof_fused.py"),
                                   "--mode", mode, "--iters", "12"], env=env, capture_output=True,

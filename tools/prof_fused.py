@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--rows", type=int, default=229376)
     ap.add_argument("--vocab", type=int, default=32000)
     ap.add_argument("--A", type=int, default=56)
+    ap.add_argument("--variant", default="none", choices=["none", "dual", "kl", "ent", "all"],
+                    help="NEXT-2 loss knobs on the fused call (readings R19-R20)")
     a = ap.parse_args()
     R, V, A = a.rows, a.vocab, a.A
     dev = "cuda"
@@ -44,8 +46,16 @@ def main():
     key = torch.ones(S, dtype=torch.int64, device=dev)
     stats = torch.zeros(24, dtype=torch.float64, device=dev)
     ws = P.workspace(1)
+    vk = {}
+    if a.variant in ("dual", "all"):
+        vk["dual_clip"] = 3.0
+    if a.variant in ("kl", "all"):
+        vk["logp_ref"] = (logp + 0.1 * torch.randn(R, generator=g, device=dev)).contiguous()
+        vk["kl_coef"] = 0.05
+    if a.variant in ("ent", "all"):
+        vk["ent_coef"] = 0.01
     fa = P.ppo_args(logp_behav=lb, adv=adv, version=ver, slot_key=key, a_tok=A, cur_version=100,
-                    tok_denominator=float(R))
+                    tok_denominator=float(R), **vk)
     gl = torch.randn(R, generator=g, device=dev) * 1e-4
 
     def call():
@@ -68,6 +78,8 @@ def main():
     torch.cuda.synchronize()
     ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(a.iters)]
     rw = {"fused": 2 * V * 2 + 12, "fwd": 2 * V + 12, "bwd": 2 * V * 2 + 12}[a.mode]
+    if a.mode == "fused" and "logp_ref" in vk:
+        rw += 4
     byt = R * rw
     avg = sum(ms) / len(ms)
     if a.mode == "fused":
@@ -76,7 +88,7 @@ def main():
         clip = st[7] / max(1.0, st[11])
     else:
         clip = None
-    print(json.dumps({"mode": a.mode, "rows": R, "vocab": V, "ms_avg": avg, "ms_min": min(ms),
+    print(json.dumps({"mode": a.mode, "variant": a.variant, "rows": R, "vocab": V, "ms_avg": avg, "ms_min": min(ms),
                       "clip_frac": clip,
                       "GBps_avg": byt / avg / 1e6, "GBps_best": byt / min(ms) / 1e6,
                       "ms_all": [round(v, 3) for v in ms]}))
