@@ -21,6 +21,9 @@ namespace {
 enum { MODE_FWD = 0, MODE_FUSED = 1, MODE_BWD = 2 };
 
 // build-time variants for A/B timing (tools/ab_variants.py); defaults are the product.
+#ifndef RLVLA_F32X2
+#define RLVLA_F32X2 1  // 0: scalar fp32 arithmetic in the TMA kernel's passes B and C
+#endif
 #ifndef RLVLA_PACKED_CLAMP
 #define RLVLA_PACKED_CLAMP 1  // 0: clamp t per element (A/B: 1 is ~1.5% faster)
 #endif
@@ -434,6 +437,54 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
       mws = (mw == -INFINITY) ? 0.f : mw;
       const float nmL = -mws * L2E;
       // ---- pass B: e = 2^(t), t = (x - m_warp) log2e; s = sum e, et = sum e t ------
+#if RLVLA_F32X2
+      // packed fp32x2 arithmetic (FFMA2 / FADD2): two columns per instruction; the
+      // thread's sums stay in two lanes of a float2 until the end of the row
+      float2 s2 = make_float2(0.f, 0.f), et2 = make_float2(0.f, 0.f);
+      const float2 L2E2 = make_float2(L2E, L2E), nmL2 = make_float2(nmL, nmL);
+#pragma unroll
+      for (int i = 0; i < kVecPerThread; ++i) {
+        const int idx = gt + i * kGroupThreads;
+        if (idx < nvec) {
+          const uint4 w = rv[idx];
+          const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
+          float2 t2[4], e2[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            // -inf -> -2^100 once per bf16 pair (NaN-propagating max): e = 0 and e t = 0
+            const uint32_t c = bmax2_nan(w4[q], kNegClampPair);
+            t2[q] = __ffma2_rn(make_float2(bf_lo(c), bf_hi(c)), L2E2, nmL2);
+            e2[q] = make_float2(ex2(t2[q].x), ex2(t2[q].y));
+          }
+          if (idx != va) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              s2 = __fadd2_rn(s2, e2[q]);
+              et2 = __ffma2_rn(e2[q], t2[q], et2);
+            }
+          } else {
+            // the target column is excluded from the sums so that 1 - p_a = S_rest/S
+            // keeps full relative precision near saturation
+            const int j0 = a & 7;
+            const int h = j0 >> 1;
+            const uint32_t wa = h == 0 ? w.x : (h == 1 ? w.y : (h == 2 ? w.z : w.w));
+            *gxa = (j0 & 1) ? bf_hi(wa) : bf_lo(wa);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if (j == j0) continue;
+              const float ej = (j & 1) ? e2[j >> 1].y : e2[j >> 1].x;
+              const float tj = (j & 1) ? t2[j >> 1].y : t2[j >> 1].x;
+              s2.x += ej;
+              et2.x = fmaf(ej, tj, et2.x);
+            }
+          }
+          if (keep_e)
+            rv[idx] = make_uint4(pack_bf16x2(e2[0].x, e2[0].y), pack_bf16x2(e2[1].x, e2[1].y),
+                                 pack_bf16x2(e2[2].x, e2[2].y), pack_bf16x2(e2[3].x, e2[3].y));
+        }
+      }
+      float s = s2.x + s2.y, et = et2.x + et2.y;
+#else
       float s = 0.f, et = 0.f;
 #pragma unroll
       for (int i = 0; i < kVecPerThread; ++i) {
@@ -495,6 +546,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
           et += vet;
         }
       }
+#endif
       s = warp_sum(s);
       et = warp_sum(et);
       if (lane == 0) gred[gw] = make_float4(mw, s, et, 0.f);
@@ -581,17 +633,32 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
             if (!kXPath) {
               // FUSED: dx = g' 2^{(m_w - M) log2e} e, e from pass B (bf16 in SMEM)
 #pragma unroll
-              for (int q = 0; q < 4; ++q) ow[q] = pack_bf16x2(kw * bf_lo(w4[q]), kw * bf_hi(w4[q]));
+              for (int q = 0; q < 4; ++q) {
+#if RLVLA_F32X2
+                const float2 d = __fmul2_rn(make_float2(bf_lo(w4[q]), bf_hi(w4[q])), make_float2(kw, kw));
+                ow[q] = pack_bf16x2(d.x, d.y);
+#else
+                ow[q] = pack_bf16x2(kw * bf_lo(w4[q]), kw * bf_hi(w4[q]));
+#endif
+              }
             } else {
               // from x: t = (x - M) log2e (lse in external bwd), dx = 2^t (k1 + k2 t);
               // -inf columns are clamped per bf16 pair so that t stays finite
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 const uint32_t c = bmax2_nan(w4[q], kNegClampPair);
+#if RLVLA_F32X2
+                const float2 t2 = __ffma2_rn(make_float2(bf_lo(c), bf_hi(c)), make_float2(L2E, L2E),
+                                             make_float2(nML, nML));
+                const float2 f2 = __ffma2_rn(make_float2(rsv.k2, rsv.k2), t2, make_float2(rsv.k1, rsv.k1));
+                const float2 d2 = __fmul2_rn(make_float2(ex2(t2.x), ex2(t2.y)), f2);
+                ow[q] = pack_bf16x2(d2.x, d2.y);
+#else
                 const float t0 = fmaf(bf_lo(c), L2E, nML);
                 const float t1 = fmaf(bf_hi(c), L2E, nML);
                 ow[q] = pack_bf16x2(ex2(t0) * fmaf(rsv.k2, t0, rsv.k1),
                                     ex2(t1) * fmaf(rsv.k2, t1, rsv.k1));
+#endif
               }
             }
             if (idx == va) {

@@ -12,8 +12,7 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
-    "lse_log1p_branch": ("RLVLA_LSE_MODE=2",),
-    "stats_first": ("RLVLA_SPLIT_STATS=0",),
+    "scalar_f32": ("RLVLA_F32X2=0",),
 }
 # name -> git revision whose csrc/ + include/ are built as one more variant
 # (the ABI only grew at the end of its structs, so today's binding drives older libraries)
