@@ -10,6 +10,8 @@
  *   S3 rlvla_logprob_fwd_bwd   action-token log-softmax + gather, forward and backward,
  *   S4                         optionally fused with the PPO / decoupled clipped surrogate
  *      rlvla_ppo_loss          the same surrogate over log-prob arrays
+ *      rlvla_value_loss        clipped value-head loss (NEXT-2)
+ *   NEXT-3 rlvla_batch_offer / rlvla_batch_poll   Eq. (1) dynamic batching on the device
  *
  * Conventions (all entry points):
  *   - Pointers are DEVICE pointers unless marked (host). Structs passed by pointer are
@@ -287,6 +289,60 @@ RLVLA_API rlvla_status rlvla_value_loss(const float* v_new, const float* v_old, 
                                         double denominator, float* grad_v, float* loss_step,
                                         double* stats, void* workspace, size_t ws_bytes,
                                         rlvla_comm comm, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * NEXT-3 — the Dynamic Batching Scheduler of Eq. (1) on the device (§3.2:
+ * "Trigger Inference if: (Batch Size >= B_max) or (Wait Time >= T_max)"; ready requests
+ * from a subset of environments enter the inference queue early). Reading R24
+ * (SPEC.md S:161-180): one rollout worker's FIFO of pending requests in
+ * arrival order; the wait clock is anchored when a request finds the queue empty and
+ * re-anchored at the poll time when a batch leaves requests behind; an empty queue never
+ * fires; more than B_max pending => the oldest B_max leave. The step just upstream of S1:
+ * it gathers the ready envs' observations into one contiguous inference batch.
+ * Times are int64 ticks (any unit; the comparison with T_max is exact).
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_env;        /* envs served by this queue (= ring capacity; an env waits for its */
+                        /* action, so it has at most one pending request)                  */
+  int64_t obs_bytes;    /* observation payload per env in bytes, multiple of 16 (0 = none) */
+  uint8_t* obs;         /* [n_env * obs_bytes] observation slots, 16-byte aligned          */
+  int32_t* ring_env;    /* [n_env] FIFO ring: env of each pending request                  */
+  int64_t* ring_time;   /* [n_env] FIFO ring: its enqueue time                             */
+  uint8_t* pending;     /* [n_env] 1 while the env has a request in the ring               */
+  int64_t* state;       /* int64[4]: head, tail (request counts since creation), anchor,   */
+                        /* number of batches emitted. Zero-filled at creation; owned by    */
+                        /* the device (the library never reads it on the host)             */
+} rlvla_batch_queue;
+
+/* Batcher counters: int64[4], ADDED to by rlvla_batch_offer (caller zeroes). */
+enum { RLVLA_BCNT_OOB = 0, RLVLA_BCNT_FUTURE = 1, RLVLA_BCNT_DUP = 2, RLVLA_BCNT_ACCEPTED = 3 };
+
+/* offer: n requests in ARRIVAL order at time `now` (>= 0), 0 <= n <= 1024 per
+ * call (split larger arrivals into consecutive calls with the same `now`: same result).
+ * Request i = (env_id[i], enqueue_time[i]); it is rejected and counted when env_id is out of
+ * [0, n_env) (OOB), when enqueue_time > now (FUTURE), or when the env already has a pending
+ * request, including an earlier accepted request of the same call (DUP); otherwise it is
+ * appended to the FIFO (ACCEPTED) and, if the queue was empty, the anchor := now.
+ * obs_src: NULL (the env side wrote its observation into obs[env] already) or device
+ * [n * obs_bytes], row i copied into obs[env_id[i]] for every accepted request.
+ * counters: device int64[4], added to. workspace: as for the other calls (>= the
+ * rlvla_workspace_bytes(0, 0, 0) header), used for its control words. */
+RLVLA_API rlvla_status rlvla_batch_offer(const rlvla_batch_queue* q, const int32_t* env_id,
+                                         const int64_t* enqueue_time, int32_t n, int64_t now,
+                                         const void* obs_src, int64_t* counters,
+                                         void* workspace, size_t ws_bytes, void* stream);
+
+/* poll (Eq. (1)): with p = pending count, the queue fires iff p >= b_max or
+ * (p >= 1 and now - anchor >= t_max); then b = min(p, b_max) oldest requests leave in FIFO
+ * order: out_env[i], out_time[i] (device [b_max]) and, if out_obs != NULL, their
+ * observations gathered into out_obs[i * obs_bytes ...] (device [b_max * obs_bytes],
+ * 16-byte aligned); remaining requests re-anchor the clock at now. *out_n (device int32)
+ * = b, 0 when the trigger does not fire (entries >= b untouched). b_max >= 1, t_max >= 0,
+ * now >= 0. The gather is one read + one write of b * obs_bytes (HBM-bound). */
+RLVLA_API rlvla_status rlvla_batch_poll(const rlvla_batch_queue* q, int64_t now, int32_t b_max,
+                                        int64_t t_max, int32_t* out_env, int64_t* out_time,
+                                        void* out_obs, int32_t* out_n, void* workspace,
+                                        size_t ws_bytes, void* stream);
 
 /* Workspace bytes for calls on buffers/logits up to these sizes (host-only, no GPU). */
 RLVLA_API size_t rlvla_workspace_bytes(int64_t rows, int32_t n_env_global, int32_t t_steps);

@@ -62,6 +62,15 @@ class c_ppo_args(ctypes.Structure):
                 ("ratio_level", c_int32)]
 
 
+BCNT_OOB, BCNT_FUTURE, BCNT_DUP, BCNT_ACCEPTED = range(4)
+
+
+class c_batch_queue(ctypes.Structure):
+    _fields_ = [("n_env", c_int32), ("obs_bytes", c_int64), ("obs", c_void_p),
+                ("ring_env", c_void_p), ("ring_time", c_void_p), ("pending", c_void_p),
+                ("state", c_void_p)]
+
+
 _SIGS = {
     "rlvla_scatter_steps": (c_int32, [POINTER(c_traj_buffer), POINTER(c_step_batch), c_int32,
                                       c_uint64, c_void_p, c_void_p]),
@@ -76,6 +85,10 @@ _SIGS = {
     "rlvla_value_loss": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
                                    c_int32, c_int32, c_float, c_double, c_void_p, c_void_p,
                                    c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
+    "rlvla_batch_offer": (c_int32, [POINTER(c_batch_queue), c_void_p, c_void_p, c_int32, c_int64,
+                                    c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "rlvla_batch_poll": (c_int32, [POINTER(c_batch_queue), c_int64, c_int32, c_int64, c_void_p,
+                                   c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "rlvla_workspace_bytes": (c_size_t, [c_int64, c_int32, c_int32]),
     "rlvla_comm_unique_id": (c_int32, [c_void_p]),
     "rlvla_comm_init": (c_int32, [c_void_p, c_int32, c_int32, POINTER(c_void_p)]),

@@ -210,6 +210,56 @@ def rlvla_value_loss(v_new, v_old, ret, slot_key, version, cur_version, grad_v, 
     return _check(st, "rlvla_value_loss", check)
 
 
+@dataclass
+class BatchQueue:
+    """rlvla_batch_queue: one rollout worker's Eq. (1) request queue (NEXT-3)."""
+    n_env: int
+    obs_bytes: int
+    obs: torch.Tensor | None   # u8 [n_env, obs_bytes] observation slots
+    ring_env: torch.Tensor     # i32 [n_env]
+    ring_time: torch.Tensor    # i64 [n_env]
+    pending: torch.Tensor      # u8 [n_env]
+    state: torch.Tensor        # i64 [4] head, tail, anchor, batches
+
+    @classmethod
+    def allocate(cls, n_env, obs_bytes=0, device="cuda"):
+        z = lambda *s, dt: torch.zeros(*s, dtype=dt, device=device)  # noqa: E731
+        obs = z(n_env, obs_bytes, dt=torch.uint8) if obs_bytes > 0 else None
+        return cls(n_env, obs_bytes, obs, z(n_env, dt=torch.int32), z(n_env, dt=torch.int64),
+                   z(n_env, dt=torch.uint8), z(4, dt=torch.int64))
+
+    def c(self) -> A.c_batch_queue:
+        return A.c_batch_queue(self.n_env, self.obs_bytes, _ptr(self.obs), _ptr(self.ring_env),
+                               _ptr(self.ring_time), _ptr(self.pending), _ptr(self.state))
+
+
+def rlvla_batch_offer(q: BatchQueue, env_id, enqueue_time, now: int, counters, *, obs_src=None,
+                      ws=None, stream=None, check=True) -> int:
+    """Offers in arrival order; more than 1024 requests go as consecutive calls with the
+    same `now` (identical semantics, see rlvla.h)."""
+    qc = q.c()
+    wp, wn = _ws_ptr(ws)
+    n = int(env_id.numel())
+    st = A.OK
+    for i0 in range(0, max(n, 1), 1024):
+        i1 = min(n, i0 + 1024)
+        src = None if obs_src is None else obs_src[i0:i1]
+        st = lib().rlvla_batch_offer(ctypes.byref(qc), _ptr(env_id[i0:i1]), _ptr(enqueue_time[i0:i1]),
+                                     i1 - i0, now, _ptr(src), _ptr(counters), wp, wn,
+                                     _stream(stream))
+        _check(st, "rlvla_batch_offer", check)
+    return st
+
+
+def rlvla_batch_poll(q: BatchQueue, now: int, b_max: int, t_max: int, out_env, out_time, out_n, *,
+                     out_obs=None, ws=None, stream=None, check=True) -> int:
+    qc = q.c()
+    wp, wn = _ws_ptr(ws)
+    st = lib().rlvla_batch_poll(ctypes.byref(qc), now, b_max, t_max, _ptr(out_env), _ptr(out_time),
+                                _ptr(out_obs), _ptr(out_n), wp, wn, _stream(stream))
+    return _check(st, "rlvla_batch_poll", check)
+
+
 def rlvla_workspace_bytes(rows: int, n_env_global: int, t_steps: int) -> int:
     return int(lib().rlvla_workspace_bytes(rows, n_env_global, t_steps))
 

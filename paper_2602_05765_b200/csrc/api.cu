@@ -314,6 +314,69 @@ RLVLA_API rlvla_status rlvla_value_loss(const float* v_new, const float* v_old, 
                          RLVLA_STAT_VALUE_DENOM - RLVLA_STAT_VALUE_LOSS, comm, s);
 }
 
+namespace {
+bool misaligned(const void* p, uintptr_t a) { return reinterpret_cast<uintptr_t>(p) % a != 0; }
+
+rlvla_status check_queue(const rlvla_batch_queue* q) {
+  if (!q || q->n_env < 1 || !q->ring_env || !q->ring_time || !q->pending || !q->state)
+    return RLVLA_ERR_INVALID_ARG;
+  if (q->obs_bytes < 0 || q->obs_bytes % 16 || (q->obs_bytes > 0 && (!q->obs || misaligned(q->obs, 16))))
+    return RLVLA_ERR_INVALID_ARG;
+  if (misaligned(q->state, 8) || misaligned(q->ring_time, 8) || misaligned(q->ring_env, 4))
+    return RLVLA_ERR_INVALID_ARG;
+  return RLVLA_OK;
+}
+
+rlvla_status check_ws(const void* workspace, size_t ws_bytes) {
+  if (!workspace || ws_bytes < ws_bytes_for(1) || misaligned(workspace, kAlignWs))
+    return RLVLA_ERR_INVALID_ARG;
+  return RLVLA_OK;
+}
+}  // namespace
+
+RLVLA_API rlvla_status rlvla_batch_offer(const rlvla_batch_queue* q, const int32_t* env_id,
+                                         const int64_t* enqueue_time, int32_t n, int64_t now,
+                                         const void* obs_src, int64_t* counters,
+                                         void* workspace, size_t ws_bytes, void* stream) {
+  rlvla_status st = check_queue(q);
+  if (st != RLVLA_OK) return st;
+  if ((st = check_ws(workspace, ws_bytes)) != RLVLA_OK) return st;
+  if (n < 0 || n > kMaxOffer || now < 0 || !counters || misaligned(counters, 8))
+    return RLVLA_ERR_INVALID_ARG;
+  if (n > 0 && (!env_id || !enqueue_time || misaligned(enqueue_time, 8))) return RLVLA_ERR_INVALID_ARG;
+  if (obs_src && misaligned(obs_src, 16)) return RLVLA_ERR_INVALID_ARG;
+  if (n == 0) return RLVLA_OK;
+  if (!device_ready()) return RLVLA_ERR_CUDA;
+  BatchOfferArgs a{*q, env_id, enqueue_time, n, now, static_cast<const uint8_t*>(obs_src),
+                   counters, carve(workspace)};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  st = cuda_status(launch_batch_offer(a, s));
+  if (st != RLVLA_OK || !sync_check_enabled()) return st;
+  int64_t c[4];
+  if (cudaMemcpyAsync(c, counters, sizeof(c), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return RLVLA_ERR_CUDA;
+  return (c[RLVLA_BCNT_OOB] || c[RLVLA_BCNT_FUTURE]) ? RLVLA_ERR_DATA : RLVLA_OK;
+}
+
+RLVLA_API rlvla_status rlvla_batch_poll(const rlvla_batch_queue* q, int64_t now, int32_t b_max,
+                                        int64_t t_max, int32_t* out_env, int64_t* out_time,
+                                        void* out_obs, int32_t* out_n, void* workspace,
+                                        size_t ws_bytes, void* stream) {
+  rlvla_status st = check_queue(q);
+  if (st != RLVLA_OK) return st;
+  if ((st = check_ws(workspace, ws_bytes)) != RLVLA_OK) return st;
+  if (b_max < 1 || t_max < 0 || now < 0 || !out_env || !out_time || !out_n)
+    return RLVLA_ERR_INVALID_ARG;
+  if (misaligned(out_time, 8) || misaligned(out_env, 4) || misaligned(out_n, 4) ||
+      (out_obs && misaligned(out_obs, 16)))
+    return RLVLA_ERR_INVALID_ARG;
+  if (!device_ready()) return RLVLA_ERR_CUDA;
+  BatchPollArgs a{*q, now, b_max, t_max, out_env, out_time, static_cast<uint8_t*>(out_obs), out_n,
+                  carve(workspace)};
+  return cuda_status(launch_batch_poll(a, static_cast<cudaStream_t>(stream)));
+}
+
 RLVLA_API rlvla_status rlvla_comm_unique_id(void* out) {
   if (!out) return RLVLA_ERR_INVALID_ARG;
   ncclUniqueId id;

@@ -17,7 +17,8 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
 // control-word indices (uint32 each) inside the workspace header
-enum { CTRL_SCATTER = 0, CTRL_ADV = 1, CTRL_LOGPROB = 2, CTRL_PPO = 3, CTRL_ADV2 = 4, CTRL_VALUE = 5 };
+enum { CTRL_SCATTER = 0, CTRL_ADV = 1, CTRL_LOGPROB = 2, CTRL_PPO = 3, CTRL_ADV2 = 4, CTRL_VALUE = 5,
+       CTRL_BOFFER = 6, CTRL_BPOLL = 7 };
 // ctrl words 32..35 hold two doubles of per-call scratch (chunk-ratio and value-loss 1/N)
 
 struct Workspace {
@@ -152,6 +153,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
+// bulk store SMEM -> global (TMA, async proxy), tracked by bulk groups
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// every committed bulk store has finished READING its shared memory
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// every committed bulk store has completed
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // small async copies (LDGSTS) whose completion arrives on an mbarrier (noinc)
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
@@ -278,5 +292,30 @@ struct ValueArgs {
   Workspace ws;
 };
 cudaError_t launch_value_loss(const ValueArgs& a, cudaStream_t s);
+
+struct BatchOfferArgs {
+  rlvla_batch_queue q;
+  const int32_t* env_id;
+  const int64_t* enqueue_time;
+  int32_t n;
+  int64_t now;
+  const uint8_t* obs_src;
+  int64_t* counters;
+  Workspace ws;
+};
+struct BatchPollArgs {
+  rlvla_batch_queue q;
+  int64_t now;
+  int32_t b_max;
+  int64_t t_max;
+  int32_t* out_env;
+  int64_t* out_time;
+  uint8_t* out_obs;
+  int32_t* out_n;
+  Workspace ws;
+};
+constexpr int kMaxOffer = 1024;
+cudaError_t launch_batch_offer(const BatchOfferArgs& a, cudaStream_t s);
+cudaError_t launch_batch_poll(const BatchPollArgs& a, cudaStream_t s);
 
 }  // namespace rlvla

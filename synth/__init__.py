@@ -426,3 +426,44 @@ def _apply_crafted(cfg, traj, env_lo, env_hi, out):
                 out[rl, cols.to(out.device)] = float("-inf")
             # "ignore": target -1 (in tokens); logits left as drawn
     return out
+
+
+# --------------------------------------------------------------------------------------
+# NEXT-3: request traffic for the Eq. (1) dynamic batching scheduler (§3.2).
+# Random draws only; the closed loop (who is batched when) is run by the caller's batcher.
+# --------------------------------------------------------------------------------------
+# OpenVLA-OFT on LIBERO: third-person + wrist 224x224 RGB uint8 images and an 8-float
+# proprio state per observation (P:99 OFT; 16-byte multiple)
+OBS_BYTES_OFT = 2 * 224 * 224 * 3 + 8 * 4
+
+
+@dataclass
+class BatcherTraffic:
+    n_env: int
+    step_ticks: np.ndarray    # i64 [n_env, n_cycles] env step durations in ticks (1 tick = 1 ms)
+    infer_ticks: np.ndarray   # i64 [n_batches_max] inference latency of the k-th batch
+    enq_lag: np.ndarray       # i64 [n_env, n_cycles] enqueue_time = offer tick - lag (0..2)
+    fault_u: np.ndarray       # f64 [ticks, 4] uniforms deciding injected bad offers per tick
+    fault_env: np.ndarray     # i64 [ticks, 4] raw env draws for those offers
+    seed: int
+
+
+def batcher_traffic(n_env: int, n_cycles: int, ticks: int, seed: int,
+                    mu: float = 3.0, sigma: float = 0.5, shift: int = 20,
+                    infer_lo: int = 5, infer_hi: int = 15) -> BatcherTraffic:
+    """Env step latencies ~ LogNormalShifted(mu, sigma, shift) ms (S:35) rounded to ticks;
+    inference latency per batch ~ U[infer_lo, infer_hi] ticks; per tick four uniforms and
+    env draws that the caller turns into bad offers (out-of-range env, future time,
+    repeated env) at its chosen rate."""
+    rng = np.random.default_rng(seed)
+    step = np.rint(shift + rng.lognormal(mu, sigma, (n_env, n_cycles))).astype(np.int64)
+    infer = rng.integers(infer_lo, infer_hi + 1, n_env * n_cycles + 1).astype(np.int64)
+    lag = rng.choice([0, 0, 0, 1, 2], size=(n_env, n_cycles)).astype(np.int64)
+    return BatcherTraffic(n_env, step, infer, lag, rng.random((ticks, 4)),
+                          rng.integers(0, 1 << 30, (ticks, 4)).astype(np.int64), seed)
+
+
+def payload_bytes(seed: int, env: int, cycle: int, obs_bytes: int) -> np.ndarray:
+    """The observation an env offers in a given cycle: seeded random bytes."""
+    r = np.random.default_rng([seed, env, cycle])
+    return r.integers(0, 256, obs_bytes, dtype=np.uint8)

@@ -179,3 +179,62 @@ def oracle_advantages(case: Case, obuf: dict, mode, **kw):
     return O_path.advantages(obuf, lv, mode=mode, group_of_env=gid,
                              cur_version=synth.CUR_VERSION, max_staleness=1,
                              env_offset=case.env_lo, **kw)
+
+
+# --------------------------------------------------------------------------------------
+# NEXT-3: closed-loop request traffic for the Eq. (1) batcher, driven by the ORACLE
+# --------------------------------------------------------------------------------------
+@dataclass
+class BatcherCase:
+    n_env: int
+    obs_bytes: int
+    b_max: int
+    t_max: int
+    ticks: list = field(default_factory=list)   # per tick: dict(now, env, time, cycle, expect)
+    counters: np.ndarray | None = None
+
+
+def batcher_case(n_env, ticks, b_max, t_max, obs_bytes=0, fault_rate=0.05, seed=7):
+    """Envs offer when their step finishes, wait for their batch, then step again after the
+    batch's inference latency; ~fault_rate of ticks carry bad offers (out-of-range env,
+    future enqueue time, a repeat of a pending env or of an env offered in the same tick).
+    The ORACLE batcher decides who is batched when; the event list (offers per tick, with
+    the payload cycle of each) and its expected batches are what the GPU replays."""
+    from oracle import batcher as O_b
+    tr = synth.batcher_traffic(n_env, 64, ticks, seed)
+    bt = O_b.Batcher(n_env)
+    nxt = tr.step_ticks[:, 0].copy()          # first offers after the first env step
+    cyc = np.zeros(n_env, np.int64)
+    nb = 0
+    case = BatcherCase(n_env, obs_bytes, b_max, t_max)
+    for now in range(ticks):
+        envs = [int(e) for e in np.nonzero(nxt == now)[0]]
+        times = [now - int(tr.enq_lag[e, cyc[e] % 64]) for e in envs]
+        cycles = [int(cyc[e]) for e in envs]
+        u, fe = tr.fault_u[now], tr.fault_env[now]
+        if u[0] < fault_rate:                                   # out of range
+            envs.append(n_env + int(fe[0] % 5)); times.append(now); cycles.append(-1)
+        if u[1] < fault_rate:                                   # enqueue time in the future
+            envs.append(int(fe[1] % n_env)); times.append(now + 1 + int(fe[1] % 3)); cycles.append(-1)
+        if u[2] < fault_rate and bt.pending.any():              # repeat of a pending env
+            pend = np.nonzero(bt.pending)[0]
+            envs.append(int(pend[fe[2] % len(pend)])); times.append(now); cycles.append(-1)
+        if u[3] < fault_rate and cycles and cycles[0] >= 0:     # same env twice in one tick
+            envs.append(envs[0]); times.append(now); cycles.append(-1)
+        bt.offer(envs, times, now)
+        batch = bt.poll(now, b_max, t_max)
+        case.ticks.append(dict(now=now, env=envs, time=times, cycle=cycles, expect=batch))
+        if batch:
+            back = now + int(tr.infer_ticks[nb])
+            nb += 1
+            for e, _ in batch:
+                cyc[e] += 1
+                nxt[e] = back + int(tr.step_ticks[e, cyc[e] % 64])
+    case.counters = bt.counters.copy()
+    return case
+
+
+def payload(case: BatcherCase, env: int, cycle: int) -> np.ndarray:
+    if cycle < 0:  # bad offers carry a recognisable filler payload
+        return np.full(case.obs_bytes, 0xEE, np.uint8)
+    return synth.payload_bytes(1234, env, cycle, case.obs_bytes)

@@ -17,7 +17,7 @@ def L():
 
 def test_exports_every_header_symbol(L):
     names = A.header_functions()
-    assert len(names) == 12
+    assert len(names) == 14
     for n in names:
         assert hasattr(L, n), n
     assert set(names) == set(A._SIGS)
@@ -38,7 +38,7 @@ def test_struct_layouts_match_header(tmp_path):
     import subprocess
     structs = {"rlvla_traj_buffer": A.c_traj_buffer, "rlvla_step_batch": A.c_step_batch,
                "rlvla_adv_params": A.c_adv_params, "rlvla_logits": A.c_logits,
-               "rlvla_ppo_args": A.c_ppo_args}
+               "rlvla_ppo_args": A.c_ppo_args, "rlvla_batch_queue": A.c_batch_queue}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "rlvla.h"', "int main(void){"]
     for cname, cls in structs.items():
         lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
@@ -135,3 +135,44 @@ def test_ppo_loss_validation(L):
     assert L.rlvla_ppo_loss(FAKE, 6, None, ctypes.byref(f), FAKE, None, None, None, 0, None, None) == A.ERR_INVALID_ARG
     f.eps_low = 1.5
     assert L.rlvla_ppo_loss(FAKE, 8, None, ctypes.byref(f), FAKE, None, None, None, 0, None, None) == A.ERR_INVALID_ARG
+
+
+def test_batcher_validation(L):
+    ws_n = L.rlvla_workspace_bytes(0, 1, 1)
+    q = A.c_batch_queue(8, 64, FAKE, FAKE, FAKE, FAKE, FAKE)
+
+    def offer(**kw):
+        return L.rlvla_batch_offer(ctypes.byref(kw.get("q", q)), kw.get("env", FAKE), kw.get("t", FAKE),
+                                   kw.get("n", 4), kw.get("now", 5), kw.get("src", None),
+                                   kw.get("cnt", FAKE), kw.get("ws", 0x100000), kw.get("wn", ws_n), None)
+
+    def poll(**kw):
+        return L.rlvla_batch_poll(ctypes.byref(kw.get("q", q)), kw.get("now", 5), kw.get("b_max", 4),
+                                  kw.get("t_max", 10), kw.get("env", FAKE), kw.get("t", FAKE),
+                                  kw.get("obs", None), kw.get("n", FAKE), kw.get("ws", 0x100000),
+                                  kw.get("wn", ws_n), None)
+
+    def qq(**kw):
+        c = A.c_batch_queue(*[getattr(q, f) for f, _ in A.c_batch_queue._fields_])
+        for k, v in kw.items():
+            setattr(c, k, v)
+        return c
+
+    assert offer(q=qq(n_env=0)) == A.ERR_INVALID_ARG
+    assert offer(q=qq(obs_bytes=24)) == A.ERR_INVALID_ARG       # not a multiple of 16
+    assert offer(q=qq(obs=None)) == A.ERR_INVALID_ARG           # payload bytes but no slots
+    assert offer(q=qq(state=FAKE + 4)) == A.ERR_INVALID_ARG     # misaligned int64 state
+    assert offer(n=1025) == A.ERR_INVALID_ARG                    # > 1024 per call
+    assert offer(n=-1) == A.ERR_INVALID_ARG
+    assert offer(now=-1) == A.ERR_INVALID_ARG
+    assert offer(env=None) == A.ERR_INVALID_ARG
+    assert offer(cnt=None) == A.ERR_INVALID_ARG
+    assert offer(src=FAKE + 8) == A.ERR_INVALID_ARG             # misaligned payload source
+    assert offer(wn=ws_n - 1) == A.ERR_INVALID_ARG
+    assert offer(n=0) == A.OK                                    # no-op, no device work
+    assert poll(b_max=0) == A.ERR_INVALID_ARG
+    assert poll(t_max=-1) == A.ERR_INVALID_ARG
+    assert poll(now=-3) == A.ERR_INVALID_ARG
+    assert poll(n=None) == A.ERR_INVALID_ARG
+    assert poll(obs=FAKE + 4) == A.ERR_INVALID_ARG
+    assert poll(ws=None) == A.ERR_INVALID_ARG

@@ -12,11 +12,13 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
-    "scalar_f32": ("RLVLA_F32X2=0",),
+    "poll256": ("RLVLA_POLL_THREADS=256",),
+    "poll_tma": ("RLVLA_POLL_TMA=1", "RLVLA_POLL_THREADS=128"),
+    "poll_tma256": ("RLVLA_POLL_TMA=1", "RLVLA_POLL_THREADS=256"),
 }
 # name -> git revision whose csrc/ + include/ are built as one more variant
 # (the ABI only grew at the end of its structs, so today's binding drives older libraries)
-REVISIONS = {"pre_next2": "6cd809f"}
+REVISIONS = {}  # e.g. {"pre_next2": "6cd809f"}
 
 
 def build_revision(name, rev):
@@ -60,15 +62,28 @@ def build():
 
 
 def run(mode="fused", rounds=3):
+    """mode: fused | fwd | bwd (tools/prof_fused.py) or batcher (tools/prof_batcher.py)."""
     res = {}
     for _ in range(rounds):
         for name in list(VARIANTS) + list(REVISIONS):
+            if not os.path.exists(os.path.join(VAR, f"{name}.so")):
+                continue
             env = dict(os.environ, RLVLA_LIB=os.path.join(VAR, f"{name}.so"))
-            out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "prof_fused.py"),
-                                  "--mode", mode, "--iters", "12"], env=env, capture_output=True,
-                                 text=True, timeout=300)
-            d = json.loads(out.stdout.strip().splitlines()[-1])
-            res.setdefault(name, []).append((round(d["ms_min"], 3), round(d["ms_avg"], 3)))
+            if mode == "batcher":
+                cmd = [sys.executable, os.path.join(ROOT, "tools", "prof_batcher.py"), "--iters", "30"]
+            else:
+                cmd = [sys.executable, os.path.join(ROOT, "tools", "prof_fused.py"), "--mode", mode,
+                       "--iters", "12"]
+            out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=300)
+            lines = out.stdout.strip().splitlines()
+            if out.returncode != 0 or not lines:
+                res.setdefault(name, []).append("failed")
+                continue
+            d = json.loads(lines[-1])
+            if mode == "batcher":
+                res.setdefault(name, []).append((round(d["poll_us_min"], 2), round(d["poll_us_median"], 2)))
+            else:
+                res.setdefault(name, []).append((round(d["ms_min"], 3), round(d["ms_avg"], 3)))
     print(json.dumps(res))
 
 
