@@ -152,6 +152,11 @@ __global__ void __launch_bounds__(kMaxOffer) batch_offer_kernel(BatchOfferArgs a
     t = a.enqueue_time[i];
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // queue state and counters: only this kernel's last CTA writes them, so every CTA may
+  // read them now, in parallel with the pending-flag loads below
+  __shared__ int64_t s_state[2], s_cnt[4];
+  if (i < 2) s_state[i] = a.q.state[i];
+  else if (i < 6) s_cnt[i - 2] = a.counters[i - 2];
   if (i < a.n) {
     if (e < 0 || e >= a.q.n_env) code = 0;
     else if (t > a.now) code = 1;
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(kMaxOffer) batch_offer_kernel(BatchOfferArgs a
   const int n_fut = __syncthreads_count(code == 1);
   const int n_dup = __syncthreads_count(code == 2);
   if (gridDim.x > 1 && !cta_is_last(a.ws.ctrl + CTRL_BOFFER)) return;
-  const int64_t head = a.q.state[0], tail = a.q.state[1];
+  const int64_t head = s_state[0], tail = s_state[1];
   if (acc) {
     const int64_t slot = (tail + pos) % a.q.n_env;
     a.q.ring_env[slot] = e;
@@ -210,10 +215,10 @@ __global__ void __launch_bounds__(kMaxOffer) batch_offer_kernel(BatchOfferArgs a
   if (i == 0) {
     if (nacc > 0 && tail == head) a.q.state[2] = a.now;  // the queue was empty: anchor
     a.q.state[1] = tail + nacc;
-    a.counters[RLVLA_BCNT_OOB] += n_oob;
-    a.counters[RLVLA_BCNT_FUTURE] += n_fut;
-    a.counters[RLVLA_BCNT_DUP] += n_dup;
-    a.counters[RLVLA_BCNT_ACCEPTED] += nacc;
+    a.counters[RLVLA_BCNT_OOB] = s_cnt[RLVLA_BCNT_OOB] + n_oob;
+    a.counters[RLVLA_BCNT_FUTURE] = s_cnt[RLVLA_BCNT_FUTURE] + n_fut;
+    a.counters[RLVLA_BCNT_DUP] = s_cnt[RLVLA_BCNT_DUP] + n_dup;
+    a.counters[RLVLA_BCNT_ACCEPTED] = s_cnt[RLVLA_BCNT_ACCEPTED] + nacc;
     a.ws.ctrl[CTRL_BOFFER] = 0u;
   }
 }
@@ -222,6 +227,7 @@ __global__ void __launch_bounds__(kPollThreads) batch_poll_kernel(BatchPollArgs 
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous call's queue updates
   const int64_t head = a.q.state[0], tail = a.q.state[1], anchor = a.q.state[2];
+  const int64_t nbatches = a.q.state[3];
   const int64_t p = tail - head;
   // Eq. (1): (Batch Size >= B_max) or (Wait Time >= T_max); an empty queue never fires
   const bool fire = p >= a.b_max || (p >= 1 && a.now - anchor >= a.t_max);
@@ -269,12 +275,13 @@ __global__ void __launch_bounds__(kPollThreads) batch_poll_kernel(BatchPollArgs 
     }
   if (gridDim.x > 1 && !cta_is_last(a.ws.ctrl + CTRL_BPOLL)) return;
   __syncthreads();
-  for (int k = threadIdx.x; k < b; k += blockDim.x) a.q.pending[a.q.ring_env[(head + k) % cap]] = 0;
+  for (int k = threadIdx.x; k < b; k += blockDim.x)
+    a.q.pending[staged ? s_env[k] : a.q.ring_env[(head + k) % cap]] = 0;
   if (threadIdx.x == 0) {
     if (b > 0) {
       a.q.state[0] = head + b;
       if (p - b > 0) a.q.state[2] = a.now;  // requests remain: re-anchor at the poll time
-      a.q.state[3] += 1;
+      a.q.state[3] = nbatches + 1;
     }
     *a.out_n = b;
     a.ws.ctrl[CTRL_BPOLL] = 0u;
