@@ -12,6 +12,7 @@
  *      rlvla_ppo_loss          the same surrogate over log-prob arrays
  *      rlvla_value_loss        clipped value-head loss (NEXT-2)
  *   NEXT-3 rlvla_batch_offer / rlvla_batch_poll   Eq. (1) dynamic batching on the device
+ *   NEXT-4 rlvla_flow_logprob  flow/diffusion chunk log-likelihood (Gaussian denoising chain)
  *
  * Conventions (all entry points):
  *   - Pointers are DEVICE pointers unless marked (host). Structs passed by pointer are
@@ -343,6 +344,44 @@ RLVLA_API rlvla_status rlvla_batch_poll(const rlvla_batch_queue* q, int64_t now,
                                         int64_t t_max, int32_t* out_env, int64_t* out_time,
                                         void* out_obs, int32_t* out_n, void* workspace,
                                         size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * NEXT-4 — flow / diffusion policies (pi_0, pi_0.5 flow matching; GR00T N1.5 diffusion:
+ * P:39, "multi-step denoising"; Table 2 "Model Num Step" = 4). Reading
+ * R25: a decision step's action chunk is the end of a K-step stochastic denoising chain
+ * with Gaussian transitions x_{k+1} ~ N(mu_theta(x_k, k), diag(sigma_{k,d}^2)); its
+ * log-likelihood is the sum of the K transition log-densities
+ *   logp_r = sum_{k,d} [ -(x - mu)^2 / (2 sigma^2) - ln sigma - ln(2 pi)/2 ],
+ * and with g_r = dLoss/dlogp_r:  dmu = g (x - mu) / sigma^2,  dln sigma = g ((x-mu)^2/sigma^2 - 1).
+ * H_r = sum_{k,d} (ln sigma + ln(2 pi e)/2) (statistics; entropy bonus through ln sigma).
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+  const void* mu;        /* [rows * n_steps * dim] denoiser means, dtype mu_dtype (row-major) */
+  int32_t mu_dtype;      /* RLVLA_F32 | RLVLA_BF16                                         */
+  const float* x;        /* [rows * n_steps * dim] the sampled next latents x_{k+1}        */
+  const float* sigma_k;  /* [n_steps] per-step std (a schedule, no gradient), used when    */
+                         /* log_std == NULL; entries must be > 0                           */
+  const float* log_std;  /* [rows * n_steps * dim] learned ln sigma, or NULL               */
+  int64_t rows;          /* decision steps                                                  */
+  int32_t n_steps, dim;  /* K denoising steps, D = chunk size x action dim                 */
+} rlvla_gauss_chain;
+
+/* Chain log-likelihood per decision step, optionally fused with the PPO surrogate and its
+ * backward (the continuous-action analogue of rlvla_logprob_fwd_bwd):
+ *   forward only  : grad_logp == NULL, fused == NULL: logp[rows] (+ stats 6..18 as in the
+ *                   forward-only logits path: N_LOSS_TOK, ENTROPY_SUM, LOGP_SUM, N_BAD_TOK)
+ *   external bwd  : grad_logp != NULL (e.g. from rlvla_ppo_loss): dmu / dlog_std from it
+ *   fused PPO     : fused != NULL, a_tok == 1 (one ratio per decision step = the chunk's
+ *                   likelihood ratio), ratio_level == 0; every PPO knob of rlvla_ppo_args
+ *                   applies (decoupled, staleness, dual clip, logp_ref KL, entropy bonus
+ *                   through ln sigma when log_std != NULL); stats slots 6..18, C3 over comm.
+ * dmu: [rows*n_steps*dim] in mu_dtype, or NULL; dlog_std: float[...] (requires log_std) or
+ * NULL. Rows with a non-finite logp are counted (N_BAD_TOK) and masked. n_steps*dim <= 4096. */
+RLVLA_API rlvla_status rlvla_flow_logprob(const rlvla_gauss_chain* c, float* logp,
+                                          const float* grad_logp, const rlvla_ppo_args* fused,
+                                          void* dmu, float* dlog_std, double* stats,
+                                          void* workspace, size_t ws_bytes, rlvla_comm comm,
+                                          void* stream);
 
 /* Workspace bytes for calls on buffers/logits up to these sizes (host-only, no GPU). */
 RLVLA_API size_t rlvla_workspace_bytes(int64_t rows, int32_t n_env_global, int32_t t_steps);

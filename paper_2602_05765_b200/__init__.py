@@ -5,8 +5,9 @@ this package is its thin binding plus host-side sharding helpers. Importing it d
 load the library; the first call does, and raises if librlvla.so has not been built.
 """
 from .api import (  # noqa: F401
-    BatchQueue, Comm, RlvlaError, StepBatch, TrajectoryBuffer, adv_params, logits_desc, ppo_args,
-    rlvla_abi_version, rlvla_advantages, rlvla_batch_offer, rlvla_batch_poll,
+    BatchQueue, Comm, GaussChain, RlvlaError, StepBatch, TrajectoryBuffer, adv_params, logits_desc,
+    ppo_args, rlvla_abi_version, rlvla_advantages, rlvla_batch_offer, rlvla_batch_poll,
+    rlvla_flow_logprob,
     rlvla_logprob_fwd_bwd, rlvla_nccl_version, rlvla_ppo_loss, rlvla_scatter_steps,
     rlvla_value_loss, rlvla_workspace_bytes, workspace)
 from . import _abi as abi  # noqa: F401

@@ -71,6 +71,11 @@ class c_batch_queue(ctypes.Structure):
                 ("state", c_void_p)]
 
 
+class c_gauss_chain(ctypes.Structure):
+    _fields_ = [("mu", c_void_p), ("mu_dtype", c_int32), ("x", c_void_p), ("sigma_k", c_void_p),
+                ("log_std", c_void_p), ("rows", c_int64), ("n_steps", c_int32), ("dim", c_int32)]
+
+
 _SIGS = {
     "rlvla_scatter_steps": (c_int32, [POINTER(c_traj_buffer), POINTER(c_step_batch), c_int32,
                                       c_uint64, c_void_p, c_void_p]),
@@ -89,6 +94,9 @@ _SIGS = {
                                     c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "rlvla_batch_poll": (c_int32, [POINTER(c_batch_queue), c_int64, c_int32, c_int64, c_void_p,
                                    c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "rlvla_flow_logprob": (c_int32, [POINTER(c_gauss_chain), c_void_p, c_void_p, POINTER(c_ppo_args),
+                                     c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p,
+                                     c_void_p]),
     "rlvla_workspace_bytes": (c_size_t, [c_int64, c_int32, c_int32]),
     "rlvla_comm_unique_id": (c_int32, [c_void_p]),
     "rlvla_comm_init": (c_int32, [c_void_p, c_int32, c_int32, POINTER(c_void_p)]),

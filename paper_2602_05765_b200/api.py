@@ -260,6 +260,33 @@ def rlvla_batch_poll(q: BatchQueue, now: int, b_max: int, t_max: int, out_env, o
     return _check(st, "rlvla_batch_poll", check)
 
 
+@dataclass
+class GaussChain:
+    """rlvla_gauss_chain (NEXT-4): K Gaussian denoising transitions per decision step."""
+    mu: torch.Tensor                    # [rows, K, D] f32 | bf16 denoiser means
+    x: torch.Tensor                     # [rows, K, D] f32 sampled x_{k+1}
+    sigma_k: torch.Tensor | None = None  # [K] f32 std schedule
+    log_std: torch.Tensor | None = None  # [rows, K, D] f32 learned ln sigma
+
+    def c(self) -> A.c_gauss_chain:
+        R, K, D = self.mu.shape
+        dt = A.BF16 if self.mu.dtype == torch.bfloat16 else A.F32
+        return A.c_gauss_chain(_ptr(self.mu), dt, _ptr(self.x), _ptr(self.sigma_k),
+                               _ptr(self.log_std), R, K, D)
+
+
+def rlvla_flow_logprob(chain: GaussChain, logp=None, grad_logp=None, fused: A.c_ppo_args | None = None,
+                       dmu=None, dlog_std=None, stats=None, ws=None, comm=None, stream=None,
+                       check=True) -> int:
+    cc = chain.c()
+    wp, wn = _ws_ptr(ws)
+    st = lib().rlvla_flow_logprob(ctypes.byref(cc), _ptr(logp), _ptr(grad_logp),
+                                  ctypes.byref(fused) if fused is not None else None, _ptr(dmu),
+                                  _ptr(dlog_std), _ptr(stats), wp, wn,
+                                  comm.handle if comm is not None else None, _stream(stream))
+    return _check(st, "rlvla_flow_logprob", check)
+
+
 def rlvla_workspace_bytes(rows: int, n_env_global: int, t_steps: int) -> int:
     return int(lib().rlvla_workspace_bytes(rows, n_env_global, t_steps))
 

@@ -377,6 +377,54 @@ RLVLA_API rlvla_status rlvla_batch_poll(const rlvla_batch_queue* q, int64_t now,
   return cuda_status(launch_batch_poll(a, static_cast<cudaStream_t>(stream)));
 }
 
+RLVLA_API rlvla_status rlvla_flow_logprob(const rlvla_gauss_chain* c, float* logp,
+                                          const float* grad_logp, const rlvla_ppo_args* fused,
+                                          void* dmu, float* dlog_std, double* stats,
+                                          void* workspace, size_t ws_bytes, rlvla_comm comm,
+                                          void* stream) {
+  if (!c || c->rows < 0 || c->n_steps < 1 || c->dim < 1 || !c->mu || !c->x)
+    return RLVLA_ERR_INVALID_ARG;
+  if (int64_t(c->n_steps) * c->dim > kFlowMaxElems) return RLVLA_ERR_INVALID_ARG;
+  if (c->mu_dtype != RLVLA_F32 && c->mu_dtype != RLVLA_BF16) return RLVLA_ERR_INVALID_ARG;
+  if (!c->log_std && !c->sigma_k) return RLVLA_ERR_INVALID_ARG;
+  if (dlog_std && !c->log_std) return RLVLA_ERR_INVALID_ARG;  // no learned ln sigma to differentiate
+  if (grad_logp && fused) return RLVLA_ERR_INVALID_ARG;
+  if (!grad_logp && !logp) return RLVLA_ERR_INVALID_ARG;
+  if (!grad_logp && !fused && (dmu || dlog_std)) return RLVLA_ERR_INVALID_ARG;  // nothing to differentiate
+  if (grad_logp && !dmu && !dlog_std) return RLVLA_ERR_INVALID_ARG;
+  if (misaligned(c->mu, c->mu_dtype == RLVLA_BF16 ? 2 : 4) || misaligned(c->x, 4) ||
+      (stats && misaligned(stats, 8)))
+    return RLVLA_ERR_INVALID_ARG;
+  if (fused) {
+    rlvla_status st = check_ppo_args(fused);
+    if (st != RLVLA_OK) return st;
+    if (fused->a_tok != 1 || fused->ratio_level != 0) return RLVLA_ERR_INVALID_ARG;
+  }
+  if (stats || fused) {
+    if (!workspace || ws_bytes < ws_bytes_for(1) || misaligned(workspace, kAlignWs))
+      return RLVLA_ERR_INVALID_ARG;
+  }
+  if (c->rows == 0) return RLVLA_OK;
+  if (!device_ready()) return RLVLA_ERR_CUDA;
+  FlowArgs a{};
+  a.c = *c;
+  a.logp = logp;
+  a.grad_logp = grad_logp;
+  a.fused = fused != nullptr;
+  if (fused) a.f = *fused;
+  a.dmu = dmu;
+  a.dlog_std = dlog_std;
+  a.stats = grad_logp ? nullptr : stats;
+  if (workspace) a.ws = carve(workspace);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  rlvla_status st = cuda_status(launch_flow(a, s));
+  if (st != RLVLA_OK || !a.stats) return st;
+  st = allreduce_stats(stats + RLVLA_STAT_LOSS, RLVLA_STAT_DENOM - RLVLA_STAT_LOSS, comm, s);
+  if (st != RLVLA_OK) return st;
+  if (sync_check_enabled()) return sync_check_stats(stats, RLVLA_STAT_N_BAD_TOK, s);
+  return RLVLA_OK;
+}
+
 RLVLA_API rlvla_status rlvla_comm_unique_id(void* out) {
   if (!out) return RLVLA_ERR_INVALID_ARG;
   ncclUniqueId id;

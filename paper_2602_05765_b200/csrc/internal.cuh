@@ -18,7 +18,7 @@ constexpr float kLn2 = 0.6931471805599453f;
 
 // control-word indices (uint32 each) inside the workspace header
 enum { CTRL_SCATTER = 0, CTRL_ADV = 1, CTRL_LOGPROB = 2, CTRL_PPO = 3, CTRL_ADV2 = 4, CTRL_VALUE = 5,
-       CTRL_BOFFER = 6, CTRL_BPOLL = 7 };
+       CTRL_BOFFER = 6, CTRL_BPOLL = 7, CTRL_FLOW = 8 };
 // ctrl words 32..35 hold two doubles of per-call scratch (chunk-ratio and value-loss 1/N)
 
 struct Workspace {
@@ -205,10 +205,15 @@ __device__ __forceinline__ bool last_block_reduce(unsigned* ctrl_word, const dou
   __syncthreads();
   if (!am_last) return false;
   __threadfence();
-  for (int s = threadIdx.x; s < nslot; s += blockDim.x) {
+  // one warp per slot: lane l sums CTAs l, l + 32, ... in order (8 loads in flight), then a
+  // fixed xor tree — deterministic for a given grid, and G/32 dependent steps instead of G
+  const int lane = threadIdx.x & 31, nw = int(blockDim.x >> 5);
+  for (int s = int(threadIdx.x >> 5); s < nslot; s += nw) {
     double acc = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) acc += __ldcg(partials + size_t(b) * RLVLA_NSTATS + s);
-    out_smem[s] = acc;
+#pragma unroll 8
+    for (unsigned b = lane; b < gridDim.x; b += 32) acc += __ldcg(partials + size_t(b) * RLVLA_NSTATS + s);
+    acc = warp_sum_d(acc);
+    if (lane == 0) out_smem[s] = acc;
   }
   __syncthreads();
   if (threadIdx.x == 0) *ctrl_word = 0u;  // leave the workspace reusable
@@ -315,6 +320,20 @@ struct BatchPollArgs {
   Workspace ws;
 };
 constexpr int kMaxOffer = 1024;
+
+struct FlowArgs {
+  rlvla_gauss_chain c;
+  float* logp;
+  const float* grad_logp;
+  int fused;
+  rlvla_ppo_args f;
+  void* dmu;
+  float* dlog_std;
+  double* stats;
+  Workspace ws;
+};
+constexpr int kFlowMaxElems = 4096;
+cudaError_t launch_flow(const FlowArgs& a, cudaStream_t s);
 cudaError_t launch_batch_offer(const BatchOfferArgs& a, cudaStream_t s);
 cudaError_t launch_batch_poll(const BatchPollArgs& a, cudaStream_t s);
 

@@ -17,7 +17,7 @@ def L():
 
 def test_exports_every_header_symbol(L):
     names = A.header_functions()
-    assert len(names) == 14
+    assert len(names) == 15
     for n in names:
         assert hasattr(L, n), n
     assert set(names) == set(A._SIGS)
@@ -38,7 +38,8 @@ def test_struct_layouts_match_header(tmp_path):
     import subprocess
     structs = {"rlvla_traj_buffer": A.c_traj_buffer, "rlvla_step_batch": A.c_step_batch,
                "rlvla_adv_params": A.c_adv_params, "rlvla_logits": A.c_logits,
-               "rlvla_ppo_args": A.c_ppo_args, "rlvla_batch_queue": A.c_batch_queue}
+               "rlvla_ppo_args": A.c_ppo_args, "rlvla_batch_queue": A.c_batch_queue,
+               "rlvla_gauss_chain": A.c_gauss_chain}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "rlvla.h"', "int main(void){"]
     for cname, cls in structs.items():
         lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
@@ -176,3 +177,34 @@ def test_batcher_validation(L):
     assert poll(n=None) == A.ERR_INVALID_ARG
     assert poll(obs=FAKE + 4) == A.ERR_INVALID_ARG
     assert poll(ws=None) == A.ERR_INVALID_ARG
+
+
+def test_flow_validation(L):
+    ws_n = L.rlvla_workspace_bytes(0, 1, 1)
+    ch = A.c_gauss_chain(FAKE, A.F32, FAKE, FAKE, None, 16, 4, 70)
+    f = A.c_ppo_args(FAKE, None, FAKE, FAKE, FAKE, 1, 100, 1, 0.2, 0.2, 0.0, 16.0, None, None, None)
+
+    def call(**kw):
+        c = A.c_gauss_chain(*[getattr(ch, k) for k, _ in A.c_gauss_chain._fields_])
+        for k, v in kw.pop("chain", {}).items():
+            setattr(c, k, v)
+        fa = kw.get("f", None)
+        return L.rlvla_flow_logprob(ctypes.byref(c), kw.get("logp", FAKE), kw.get("g", None),
+                                    ctypes.byref(fa) if fa is not None else None, kw.get("dmu", None),
+                                    kw.get("dls", None), kw.get("stats", None), kw.get("ws", 0x100000),
+                                    kw.get("wn", ws_n), None, None)
+
+    assert call(chain=dict(n_steps=0)) == A.ERR_INVALID_ARG
+    assert call(chain=dict(n_steps=64, dim=65)) == A.ERR_INVALID_ARG      # K*D > 4096
+    assert call(chain=dict(mu_dtype=7)) == A.ERR_INVALID_ARG
+    assert call(chain=dict(sigma_k=None)) == A.ERR_INVALID_ARG            # no sigma at all
+    assert call(dls=FAKE) == A.ERR_INVALID_ARG                            # dlog_std w/o log_std
+    assert call(logp=None) == A.ERR_INVALID_ARG
+    assert call(dmu=FAKE) == A.ERR_INVALID_ARG                            # forward-only + grads
+    assert call(g=FAKE, f=f) == A.ERR_INVALID_ARG                         # two gradient sources
+    assert call(g=FAKE) == A.ERR_INVALID_ARG                              # external bwd w/o outputs
+    bad = A.c_ppo_args(*[getattr(f, k) for k, _ in A.c_ppo_args._fields_])
+    bad.a_tok = 7
+    assert call(f=bad, dmu=FAKE) == A.ERR_INVALID_ARG                     # one ratio per step
+    assert call(f=f, dmu=FAKE, ws=None) == A.ERR_INVALID_ARG
+    assert call(chain=dict(rows=0)) == A.OK

@@ -12,9 +12,8 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
-    "poll256": ("RLVLA_POLL_THREADS=256",),
-    "poll_tma": ("RLVLA_POLL_TMA=1", "RLVLA_POLL_THREADS=128"),
-    "poll_tma256": ("RLVLA_POLL_TMA=1", "RLVLA_POLL_THREADS=256"),
+    "flow_t8": ("RLVLA_FLOW_TILE=8",),
+    "flow_m3": ("RLVLA_FLOW_MINB=3",),
 }
 # name -> git revision whose csrc/ + include/ are built as one more variant
 # (the ABI only grew at the end of its structs, so today's binding drives older libraries)
@@ -71,6 +70,8 @@ def run(mode="fused", rounds=3):
             env = dict(os.environ, RLVLA_LIB=os.path.join(VAR, f"{name}.so"))
             if mode == "batcher":
                 cmd = [sys.executable, os.path.join(ROOT, "tools", "prof_batcher.py"), "--iters", "30"]
+            elif mode == "flow":
+                cmd = [sys.executable, os.path.join(ROOT, "tools", "prof_flow.py"), "--rows", "196608"]
             else:
                 cmd = [sys.executable, os.path.join(ROOT, "tools", "prof_fused.py"), "--mode", mode,
                        "--iters", "12"]
@@ -82,6 +83,8 @@ def run(mode="fused", rounds=3):
             d = json.loads(lines[-1])
             if mode == "batcher":
                 res.setdefault(name, []).append((round(d["poll_us_min"], 2), round(d["poll_us_median"], 2)))
+            elif mode == "flow":
+                res.setdefault(name, []).append((round(d["us_min"], 1), round(d["us_median"], 1)))
             else:
                 res.setdefault(name, []).append((round(d["ms_min"], 3), round(d["ms_avg"], 3)))
     print(json.dumps(res))
