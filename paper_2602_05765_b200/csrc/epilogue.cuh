@@ -166,6 +166,21 @@ __device__ __forceinline__ void acc_stats(double* acc, const RowStats& rs) {
   acc[11] += double(rs.pg);
 }
 
+__device__ __forceinline__ void acc_stats_f(float* acc, const RowStats& rs) {
+  acc[0] += rs.loss;
+  acc[1] += rs.clipped;
+  acc[2] += rs.k3;
+  acc[3] += rs.ent;
+  acc[4] += rs.rho;
+  acc[5] += rs.m;
+  acc[6] += rs.stale;
+  acc[7] += rs.bad;
+  acc[8] += rs.logp;
+  acc[9] += rs.kl_ref;
+  acc[10] += rs.dual;
+  acc[11] += rs.pg;
+}
+
 // N for the 1/N normalisation: explicit, else the global token count from rlvla_advantages
 __device__ __forceinline__ double loss_denominator(double denom, const double* adv_stats) {
   if (denom > 0.0) return denom;

@@ -88,6 +88,7 @@ __device__ __forceinline__ void row_partials(const FlowArgs& a, const float* s_i
   q = 0.f;
   ls = 0.f;
   if (VEC) {
+    float2 q2 = make_float2(0.f, 0.f);
     for (int j = 4 * lane; j < n; j += 128) {
       const float4 m = ld_mu4<T>(mu, j);
       const float4 xv = *reinterpret_cast<const float4*>(x + j);
@@ -99,10 +100,14 @@ __device__ __forceinline__ void row_partials(const FlowArgs& a, const float* s_i
       } else {
         iv = *reinterpret_cast<const float4*>(s_isig + j);
       }
-      const float z0 = (xv.x - m.x) * iv.x, z1 = (xv.y - m.y) * iv.y;
-      const float z2 = (xv.z - m.z) * iv.z, z3 = (xv.w - m.w) * iv.w;
-      q = fmaf(z0, z0, fmaf(z1, z1, fmaf(z2, z2, fmaf(z3, z3, q))));
+      // packed fp32x2 (FADD2 / FMUL2 / FFMA2): two elements per instruction
+      const float2 za = __fmul2_rn(__fadd2_rn(make_float2(xv.x, xv.y), make_float2(-m.x, -m.y)),
+                                   make_float2(iv.x, iv.y));
+      const float2 zb = __fmul2_rn(__fadd2_rn(make_float2(xv.z, xv.w), make_float2(-m.z, -m.w)),
+                                   make_float2(iv.z, iv.w));
+      q2 = __ffma2_rn(za, za, __ffma2_rn(zb, zb, q2));
     }
+    q = q2.x + q2.y;
   } else {
     for (int j = lane; j < n; j += 32) {
       const float m = ld_mu<T>(mu, j);
@@ -143,9 +148,13 @@ __device__ __forceinline__ void row_backward(const FlowArgs& a, const float* s_i
         } else {
           iv = *reinterpret_cast<const float4*>(s_isig + j);
         }
-        const float z0 = (xv.x - m.x) * iv.x, z1 = (xv.y - m.y) * iv.y;
-        const float z2 = (xv.z - m.z) * iv.z, z3 = (xv.w - m.w) * iv.w;
-        dm = make_float4(g * z0 * iv.x, g * z1 * iv.y, g * z2 * iv.z, g * z3 * iv.w);
+        const float2 ia = make_float2(iv.x, iv.y), ib = make_float2(iv.z, iv.w);
+        const float2 za = __fmul2_rn(__fadd2_rn(make_float2(xv.x, xv.y), make_float2(-m.x, -m.y)), ia);
+        const float2 zb = __fmul2_rn(__fadd2_rn(make_float2(xv.z, xv.w), make_float2(-m.z, -m.w)), ib);
+        const float2 g2 = make_float2(g, g);
+        const float2 da = __fmul2_rn(__fmul2_rn(g2, za), ia), db = __fmul2_rn(__fmul2_rn(g2, zb), ib);
+        dm = make_float4(da.x, da.y, db.x, db.y);
+        const float z0 = za.x, z1 = za.y, z2 = zb.x, z3 = zb.y;
         if (dls)
           dl = make_float4(fmaf(g, fmaf(z0, z0, -1.f), -c), fmaf(g, fmaf(z1, z1, -1.f), -c),
                            fmaf(g, fmaf(z2, z2, -1.f), -c), fmaf(g, fmaf(z3, z3, -1.f), -c));
@@ -217,7 +226,9 @@ __global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(
     Nden = loss_denominator(a.f.tok_denominator, a.f.adv_stats);
     pc.invN = Nden > 0.0 ? float(1.0 / Nden) : 0.f;
   }
-  double acc[kLossSlots] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  // per-lane statistics of the few rows this lane owns in fp32 (deterministic order); the
+  // warp, CTA and grid reductions are fp64
+  float acc[kLossSlots] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   const int64_t ntiles = (a.c.rows + kTile - 1) / kTile;
   const int64_t gw = int64_t(blockIdx.x) * kFlowWarps + warp, nw = int64_t(gridDim.x) * kFlowWarps;
   for (int64_t tile = gw; tile < ntiles; tile += nw) {
@@ -281,7 +292,7 @@ __global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(
           fwd_row_stats(in, rs);
         }
         if (a.logp) a.logp[r] = logp;
-        if (want_stats) acc_stats(acc, rs);
+        if (want_stats) acc_stats_f(acc, rs);
       }
       __syncwarp();  // the partials are read before the next tile overwrites them
     } else {
@@ -299,9 +310,10 @@ __global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(
   if (!want_stats) return;
   __shared__ double red[kFlowWarps][kLossSlots];
   __shared__ double cta[kLossSlots];
-  for (int k = 0; k < kLossSlots; ++k) acc[k] = warp_sum_d(acc[k]);
+  double accd[kLossSlots];
+  for (int k = 0; k < kLossSlots; ++k) accd[k] = warp_sum_d(double(acc[k]));
   if (lane == 0)
-    for (int k = 0; k < kLossSlots; ++k) red[warp][k] = acc[k];
+    for (int k = 0; k < kLossSlots; ++k) red[warp][k] = accd[k];
   __syncthreads();
   if (threadIdx.x < kLossSlots) {
     double sm = 0;
