@@ -21,6 +21,9 @@ namespace {
 enum { MODE_FWD = 0, MODE_FUSED = 1, MODE_BWD = 2 };
 
 // build-time variants for A/B timing (tools/ab_variants.py); defaults are the product.
+#ifndef RLVLA_NFULL_FUSED
+#define RLVLA_NFULL_FUSED 0  // A/B: unchecked vectors cost the fused kernel 4-5% (one spill at 64 regs)
+#endif
 #ifndef RLVLA_F32X2
 #define RLVLA_F32X2 1  // 0: scalar fp32 arithmetic in the TMA kernel's passes B and C
 #endif
@@ -350,7 +353,9 @@ __device__ __forceinline__ void scalars_sync(int g) {
 // XP: pass C from x (external bwd, or fused with the entropy bonus); otherwise from the e
 // values pass B kept in the stage. A template parameter so the common fused loop carries
 // no code of the other.
-template <int MODE, bool XP>
+// NFULL: the first NFULL of a thread's kVecPerThread vectors are always inside the row
+// (NFULL = nvec / 512), so those iterations carry no bounds check.
+template <int MODE, bool XP, int NFULL>
 __global__ void __launch_bounds__(kCtaThreads, 1)
     lp_tma_kernel(Lp p, int nstages, uint32_t stage_bytes) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -376,6 +381,12 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
   // pass C runs in external-bwd mode and in fused mode with dlogits; it reuses the e
   // values of pass B (stored as bf16 in the stage) unless the entropy bonus needs x
   constexpr bool kXPath = XP || MODE == MODE_BWD;
+  // forward: the target column is removed from the pass-B sums by overwriting it with -inf
+  // after pass A (branch-free loop); fused: skipped inside the loop of its owner thread
+#ifndef RLVLA_NEGINF_FUSED
+#define RLVLA_NEGINF_FUSED 0
+#endif
+  constexpr bool kNegInfTarget = MODE == MODE_FWD || (MODE == MODE_FUSED && RLVLA_NEGINF_FUSED);
   const bool has_c = MODE == MODE_BWD || (MODE == MODE_FUSED && p.dx != nullptr);
   const bool keep_e = MODE == MODE_FUSED && !kXPath && p.dx != nullptr;
   const float L2E = kLog2e;
@@ -416,6 +427,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     const int a = mt->a;
     const bool tgt_ok = unsigned(a) < unsigned(V);
     const int va = tgt_ok ? (a >> 3) : -1;
+    const bool owner = tgt_ok && (va & (kGroupThreads - 1)) == gt;  // thread holding the target
     // warp partials double-buffered by row parity: rows k and k+2 of a group never share
     float4* gred = red + (((k >> 1) & 1) * 2 + grp) * kGroupWarps;
     float* gxa = xa_s + ((k >> 1) & 1) * 2 + grp;  // raw target logit, same double buffering
@@ -428,10 +440,18 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
 #pragma unroll
       for (int i = 0; i < kVecPerThread; ++i) {
         const int idx = gt + i * kGroupThreads;
-        if (idx < nvec) {
+        if (i < NFULL || idx < nvec) {
           const uint4 w = rv[idx];
           mm = bmax2(bmax2(mm, w.x), bmax2(w.y, bmax2(w.z, w.w)));
         }
+      }
+      // The target column is excluded from the pass-B sums (so that 1 - p_a = S_rest / S
+      // keeps full relative precision near saturation) by overwriting it with -inf in the
+      // stage once the max has seen it; only its owner thread reads that vector again.
+      if ((kNegInfTarget || !RLVLA_F32X2) && owner) {
+        uint16_t* hx = reinterpret_cast<uint16_t*>(row);
+        *gxa = bf_lo(uint32_t(hx[a]));
+        hx[a] = 0xFF80u;
       }
       const float mw = warp_max(fmaxf(bf_lo(mm), bf_hi(mm)));
       mws = (mw == -INFINITY) ? 0.f : mw;
@@ -445,26 +465,27 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
 #pragma unroll
       for (int i = 0; i < kVecPerThread; ++i) {
         const int idx = gt + i * kGroupThreads;
-        if (idx < nvec) {
+        if (i < NFULL || idx < nvec) {
           const uint4 w = rv[idx];
           const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
           float2 t2[4], e2[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             // -inf -> -2^100 once per bf16 pair (NaN-propagating max): e = 0 and e t = 0
+            // (this also removes the target column, set to -inf after pass A)
             const uint32_t c = bmax2_nan(w4[q], kNegClampPair);
             t2[q] = __ffma2_rn(make_float2(bf_lo(c), bf_hi(c)), L2E2, nmL2);
             e2[q] = make_float2(ex2(t2[q].x), ex2(t2[q].y));
           }
-          if (idx != va) {
+          if (kNegInfTarget || idx != va) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               s2 = __fadd2_rn(s2, e2[q]);
               et2 = __ffma2_rn(e2[q], t2[q], et2);
             }
           } else {
-            // the target column is excluded from the sums so that 1 - p_a = S_rest/S
-            // keeps full relative precision near saturation
+            // fused kernel: the target column is skipped here instead (A/B: the -inf
+            // overwrite costs the fused kernel ~1.5%, it saves the forward 11%)
             const int j0 = a & 7;
             const int h = j0 >> 1;
             const uint32_t wa = h == 0 ? w.x : (h == 1 ? w.y : (h == 2 ? w.z : w.w));
@@ -489,7 +510,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
 #pragma unroll
       for (int i = 0; i < kVecPerThread; ++i) {
         const int idx = gt + i * kGroupThreads;
-        if (idx < nvec) {
+        if (i < NFULL || idx < nvec) {
           const uint4 w = rv[idx];
           const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
           float e[8];
@@ -522,23 +543,6 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
             vet = fmaf(e[2 * q + 1], fmaxf(t1, -256.f), vet);
           }
 #endif
-          if (idx == va) {
-            // the target column is excluded from the sums so that 1 - p_a = S_rest/S
-            // keeps full relative precision near saturation; recompute this vector
-            const int j0 = a & 7;
-            const int h = j0 >> 1;
-            const uint32_t wa = h == 0 ? w.x : (h == 1 ? w.y : (h == 2 ? w.z : w.w));
-            *gxa = (j0 & 1) ? bf_hi(wa) : bf_lo(wa);
-            vs = 0.f;
-            vet = 0.f;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              if (j == j0) continue;
-              const float t = fmaf(j & 1 ? bf_hi(w4[j >> 1]) : bf_lo(w4[j >> 1]), L2E, nmL);
-              vs += e[j];
-              vet = fmaf(e[j], fmaxf(t, -256.f), vet);
-            }
-          }
           if (keep_e)
             rv[idx] = make_uint4(pack_bf16x2(e[0], e[1]), pack_bf16x2(e[2], e[3]),
                                  pack_bf16x2(e[4], e[5]), pack_bf16x2(e[6], e[7]));
@@ -614,6 +618,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
       rsv.ga = tgt_ok ? -g * expm1f(bf_lo(uint32_t(reinterpret_cast<const uint16_t*>(row)[a])) - mt->lse_in)
                       : 0.f;
       rsv.active = g != 0.f ? 1.f : 0.f;
+      if (owner) reinterpret_cast<uint16_t*>(row)[a] = 0xFF80u;  // target column written last
     }
 
     // ---- pass C: dlogits (masked / clipped rows get exact zeros) ---------------------
@@ -624,7 +629,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
 #pragma unroll
       for (int i = 0; i < kVecPerThread; ++i) {
         const int idx = gt + i * kGroupThreads;
-        if (idx < nvec) {
+        if (i < NFULL || idx < nvec) {
           uint4 o = make_uint4(0u, 0u, 0u, 0u);
           if (rsv.active != 0.f) {
             const uint4 w = rv[idx];
@@ -661,7 +666,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
 #endif
               }
             }
-            if (idx == va) {
+            if (idx == va) {  // the target column (0 from its -inf) takes g (1 - p_a) [+ ...]
               const uint32_t hb = uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(rsv.ga)));
               const int qd = (a & 7) >> 1, hf = a & 1;
 #pragma unroll
@@ -965,21 +970,32 @@ cudaError_t launch_mode(const LpArgs& a, Lp p, cudaStream_t s) {
     const size_t smem = size_t(nst) * stage_bytes + fixed;
     // dynamic smem limit = opt-in max minus the kernel's static smem
     const bool xp = MODE == MODE_FUSED && a.f.ent_coef != 0.f && a.dlogits != nullptr;
-    const void* fn = xp ? reinterpret_cast<const void*>(lp_tma_kernel<MODE, true>)
-                        : reinterpret_cast<const void*>(lp_tma_kernel<MODE, false>);
-    static int attr_dyn[3][2] = {{0, 0}, {0, 0}, {0, 0}};
-    if (attr_dyn[MODE][xp] < int(smem)) {
+    const int nvec = a.x.vocab >> 3;
+    // V > 28672 (OpenVLA 32000): 7 unchecked vectors (RLVLA_NFULL_FUSED=0 keeps the checks in
+    // the fused kernel)
+    const bool f7 = nvec / kGroupThreads >= 7 && (MODE != MODE_FUSED || RLVLA_NFULL_FUSED);
+    const void* fn = xp ? (f7 ? reinterpret_cast<const void*>(lp_tma_kernel<MODE, true, 7>)
+                              : reinterpret_cast<const void*>(lp_tma_kernel<MODE, true, 0>))
+                        : (f7 ? reinterpret_cast<const void*>(lp_tma_kernel<MODE, false, 7>)
+                              : reinterpret_cast<const void*>(lp_tma_kernel<MODE, false, 0>));
+    static int attr_dyn[3][2][2] = {};
+    if (attr_dyn[MODE][xp][f7] < int(smem)) {
       cudaFuncAttributes fa{};
       cudaError_t e = cudaFuncGetAttributes(&fa, fn);
       if (e != cudaSuccess) return e;
       if (smem + fa.sharedSizeBytes > size_t(device_info().smem_optin)) return cudaErrorInvalidConfiguration;
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
-      attr_dyn[MODE][xp] = int(smem);
+      attr_dyn[MODE][xp][f7] = int(smem);
     }
     int grid = int(R < sms ? R : sms);
-    if (xp) lp_tma_kernel<MODE, true><<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);
-    else lp_tma_kernel<MODE, false><<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);
+    if (xp) {
+      if (f7) lp_tma_kernel<MODE, true, 7><<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);
+      else lp_tma_kernel<MODE, true, 0><<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);
+    } else {
+      if (f7) lp_tma_kernel<MODE, false, 7><<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);
+      else lp_tma_kernel<MODE, false, 0><<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);
+    }
     return cudaGetLastError();
   }
   if (path == LP_PATH_WARP) {
