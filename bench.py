@@ -398,6 +398,12 @@ def run_ours(args):
                                            n_env_sample=min(2, mb_envs))
     if rank == 0:
         print(json.dumps(out), flush=True)
+    # the captured graph holds NCCL's persistent plans for the C1/C2/C3 collectives: release
+    # it before the communicator, or ncclCommDestroy waits for them forever
+    graph = None
+    import gc
+    gc.collect()
+    torch.cuda.synchronize()
     if comm is not None:
         comm.destroy()
     if world > 1:

@@ -2,7 +2,8 @@
 each rank scatters the records it owns, computes GRPO (groups spanning ranks: C2
 allgather + C1 allreduce) and GAE+global whitening advantages, and the fused loss with the
 C3 allreduce, all through the C ABI with the library's NCCL communicator; the result is
-compared with the oracle on the same shard using the same sharding helpers.
+compared with the oracle on the same shard using the same sharding helpers. Then the value
+loss (slots 19..21) and the flow-policy chain loss (C3) with a global denominator.
 
   torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/mgpu_parity.py
 """
@@ -120,6 +121,51 @@ def main():
     assert abs(s3[6] - rs[0]) <= 1e-5 * max(1e-3, abs(rs[0])), (s3[6], rs[0])
     assert s3[11] == rs[1] and abs(s3[9] - rs[2]) <= 1e-5 * abs(rs[2])
     assert s3[18] == tot[1].item()
+    # NEXT-2 value loss: per-rank steps, explicit global N_v, slots 19..21 allreduced
+    from oracle import flow as O_fl
+    from oracle import ppo as O_ppo
+    rng = np.random.default_rng(100 + rank)
+    nv = 3000
+    v, vo, Rt = (rng.normal(size=nv).astype(np.float32) for _ in range(3))
+    key = np.where(rng.random(nv) < 0.9, 1, 0).astype(np.int64)
+    ver = np.full(nv, CUR, np.int32)
+    Nv = float(world * nv)
+    gv = torch.empty(nv, device=dev)
+    st4 = torch.zeros(24, dtype=torch.float64, device=dev)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    P.rlvla_value_loss(cu(v), cu(vo), cu(Rt), cu(key), cu(ver), CUR, gv, clip_eps=0.2, denominator=Nv,
+                       stats=st4, ws=ws, comm=comm)
+    o = O_ppo.value_loss(v, vo, Rt, key != 0, clip_eps=0.2, n_den=Nv)
+    H.assert_close_rel(gv.cpu().numpy(), o["grad"], 1e-5, 1e-9, "value grad")
+    rv = torch.tensor([o["stats"]["loss"], float((key != 0).sum())], dtype=torch.float64, device=dev)
+    dist.all_reduce(rv)
+    s4 = st4.cpu().numpy()
+    assert abs(s4[19] - rv[0].item()) <= 1e-5 * abs(rv[0].item()) and s4[21] == rv[1].item()
+    # NEXT-4 flow chain + PPO: one ratio per step, C3 over the ranks
+    Rf, K, Df = 200, 4, 70
+    sig = np.array([0.8, 0.5, 0.3, 0.1], np.float32)
+    mu = rng.normal(size=(Rf, K, Df)).astype(np.float32)
+    xf = (mu + sig[None, :, None] * rng.normal(size=(Rf, K, Df))).astype(np.float32)
+    lp = O_fl.chain_logprob(mu, xf, sigma_k=sig)["logp"]
+    lb = (lp - rng.normal(0, 0.05, Rf)).astype(np.float32)
+    advf = rng.normal(size=Rf).astype(np.float32)
+    Nf = float(world * Rf)
+    gf = torch.empty(Rf, device=dev)
+    st5 = torch.zeros(24, dtype=torch.float64, device=dev)
+    fa = P.ppo_args(logp_behav=cu(lb), adv=cu(advf), version=cu(np.full(Rf, CUR, np.int32)),
+                    slot_key=cu(np.ones(Rf, np.int64)), a_tok=1, cur_version=CUR, tok_denominator=Nf,
+                    out_grad_logp=gf)
+    ch = P.GaussChain(cu(mu), cu(xf), cu(sig))
+    P.rlvla_flow_logprob(ch, logp=torch.empty(Rf, device=dev), fused=fa, dmu=torch.empty_like(ch.mu),
+                         stats=st5, ws=ws, comm=comm)
+    pf = O_ppo.ppo_loss(lp, lb, advf, np.ones(Rf, bool), np.zeros(Rf, int), n_tok=Nf)
+    ok = ~pf["near_tie"]
+    H.assert_close_rel(gf.cpu().numpy()[ok], pf["grad"][ok], 1e-4, 1e-6, "flow grad")
+    rf = torch.tensor([pf["stats"]["loss"], float(Rf)], dtype=torch.float64, device=dev)
+    dist.all_reduce(rf)
+    s5 = st5.cpu().numpy()
+    assert abs(s5[6] - rf[0].item()) <= 1e-4 * max(1e-3, abs(rf[0].item())), (s5[6], rf[0].item())
+    assert s5[11] == rf[1].item() and s5[18] == Nf
     dist.barrier()
     if rank == 0:
         print(f"MGPU PARITY OK world={world} nccl={P.rlvla_nccl_version()}", flush=True)
