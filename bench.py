@@ -242,6 +242,10 @@ def run_ours(args):
     ev_k0 = [cr.event() for _ in range(args.steps * nmb)]
     ev_k1 = [cr.event() for _ in range(args.steps * nmb)]
     ev_t0, ev_t1 = cr.event(), cr.event()
+    # per-stage events (S1/S2 are latency-bound, reported in us per call)
+    ev_sa = [cr.event() for _ in range(args.steps)]   # before the scatter calls
+    ev_sb = [cr.event() for _ in range(args.steps)]   # after the scatter calls
+    ev_sc = [cr.event() for _ in range(args.steps)]   # after rlvla_advantages
 
     def step(i=None, capturing=False):
         stream = torch.cuda.current_stream()
@@ -249,10 +253,16 @@ def run_ours(args):
         buf.reset()
         counters.zero_()
         seq = 1
+        if i is not None:
+            cr.record(ev_sa[i], sh, capturing)
         for sl, cb in zip(chunks, chunk_batches):
             P.rlvla_scatter_steps(buf, cb, synth.CUR_VERSION, seq, counters, stream=stream)
             seq += sl.stop - sl.start
+        if i is not None:
+            cr.record(ev_sb[i], sh, capturing)
         P.rlvla_advantages(buf, lv, prm, adv, ret, stats, ws, comm=comm, stream=stream)
+        if i is not None:
+            cr.record(ev_sc[i], sh, capturing)
         for j, ((m0, m1), fa) in enumerate(zip(mbs, fas)):
             if i is not None:
                 cr.record(ev_k0[i * nmb + j], sh, capturing)
@@ -306,6 +316,8 @@ def run_ours(args):
     clocks = clk.stop()
     ms = cr.elapsed(ev_t0, ev_t1)
     k_ms = [cr.elapsed(a, b) for a, b in zip(ev_k0, ev_k1)]   # one per fused launch
+    sc_ms = sorted(cr.elapsed(a, b) for a, b in zip(ev_sa, ev_sb))
+    ad_ms = sorted(cr.elapsed(a, b) for a, b in zip(ev_sb, ev_sc))
     st_host = lstats.cpu().numpy()
     cnt = counters.cpu().numpy()
 
@@ -384,8 +396,16 @@ def run_ours(args):
         "gpu_launches": launches_per_step * args.steps,
         "gpu_launches_per_step": {"scatter": len(chunks), "advantages": n_adv_kernels,
                                   "fused_logprob_ppo": nmb},
+        "stages": {"scatter_us_per_step_median": 1e3 * sc_ms[len(sc_ms) // 2],
+                   "scatter_calls_per_step": len(chunks),
+                   "scatter_us_per_call_median": 1e3 * sc_ms[len(sc_ms) // 2] / max(1, len(chunks)),
+                   "advantages_us_median": 1e3 * ad_ms[len(ad_ms) // 2],
+                   "advantages_ns_per_env_step": 1e6 * ad_ms[len(ad_ms) // 2] / (units_per_step / world),
+                   "fused_ms_per_step_median": sorted(k_ms)[len(k_ms) // 2] * nmb,
+                   "note": "CUDA event nodes inside the timed graph; S1/S2 latency-bound (us per call)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
+                     "peak_nominal": 8000.0, "frac_nominal": achieved / 8000.0,
                      "kernel": "lp_tma_kernel<FUSED> (rlvla_logprob_fwd_bwd fused)",
                      "kernel_ms": k_avg, "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
                      "kernel_share_of_step": k_avg * nmb / (ms / args.steps)},
@@ -436,12 +456,25 @@ def oracle_sample_step(cfg, traj, logits_rows_fn, n_env_sample):
     return time.perf_counter() - t
 
 
+def host_cpu() -> str:
+    """The GPU box's host CPU (model name, logical cores) for the oracle baseline."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return f"{model}, {os.cpu_count()} logical cores"
+
+
 def cpu_baseline(cfg, traj, logits, lb_fn=None, n_env_sample=2):
     def rows_fn(n):
         return logits[: n * cfg.t_steps * cfg.a_tok].double().cpu().numpy()
     sec = oracle_sample_step(cfg, traj, rows_fn, n_env_sample)
     units = n_env_sample * cfg.n_es
-    return {"value": units / sec, "unit": UNIT, "cores": 1, "kind": "oracle",
+    return {"value": units / sec, "unit": UNIT, "cores": 1, "kind": "oracle", "host": host_cpu(),
             "sample": f"{n_env_sample} of {cfg.n_env} envs x {cfg.n_es} env steps "
                       f"({n_env_sample * cfg.t_steps * cfg.a_tok} logit rows x {cfg.vocab}), "
                       f"whole path S1-S4, numpy fp64 single thread, {sec:.1f} s"}
@@ -472,7 +505,7 @@ def run_reference(args):
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": cfg.name, "envs_per_step": n, "vocab": cfg.vocab,
                       "parallelism": "cpu oracle (rank 0 only)"},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "host": host_cpu(),
                             "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "gpu_launches": 0}
