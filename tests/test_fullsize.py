@@ -116,3 +116,84 @@ def test_fullsize_rerun_bit_identical(full):
     torch.cuda.synchronize()
     assert torch.equal(dx2, full["dx"]) and torch.equal(logp2, full["logp"])
     assert torch.equal(st, full["st2"])
+
+
+def test_fullsize_flow_sampled_rows():
+    """NEXT-4 at the prof_flow.py launch size (196,608 pi_0 decision steps, K 4 x D 70,
+    bf16 means, fused PPO + backward): sampled steps against the oracle, every step's
+    gradient row consistent with its own g (dmu * sigma^2 / (x - mu) == g), stats = fp64 sum
+    of the per-step outputs."""
+    import paper_2602_05765_b200 as P
+    from oracle import flow as O_fl
+    from oracle import ppo as O_ppo
+    R, K, D = 196608, 4, 70
+    g0 = torch.Generator(device="cuda").manual_seed(5)
+    sig = torch.tensor([0.8, 0.5, 0.3, 0.1], device="cuda")
+    mu = torch.randn(R, K, D, generator=g0, device="cuda").to(torch.bfloat16)
+    x = (mu.float() + sig.view(1, K, 1) * torch.randn(R, K, D, generator=g0, device="cuda")).contiguous()
+    ch = P.GaussChain(mu, x, sig)
+    lp0 = torch.empty(R, device="cuda")
+    P.rlvla_flow_logprob(ch, logp=lp0)
+    lb = (lp0 + 0.05 * torch.randn(R, generator=g0, device="cuda")).contiguous()
+    adv = torch.randn(R, generator=g0, device="cuda")
+    ver = torch.full((R,), 100, dtype=torch.int32, device="cuda")
+    key = torch.ones(R, dtype=torch.int64, device="cuda")
+    g = torch.empty(R, device="cuda")
+    fa = P.ppo_args(logp_behav=lb, adv=adv, version=ver, slot_key=key, a_tok=1, cur_version=100,
+                    tok_denominator=float(R), out_grad_logp=g)
+    logp = torch.empty(R, device="cuda")
+    dmu = torch.empty_like(mu)
+    st = torch.zeros(24, dtype=torch.float64, device="cuda")
+    P.rlvla_flow_logprob(ch, logp=logp, fused=fa, dmu=dmu, stats=st, ws=P.workspace(1))
+    torch.cuda.synchronize()
+    assert torch.equal(logp, lp0)                                   # same sums in both modes
+    rows = np.random.default_rng(0).choice(R, 256, replace=False)
+    rt = torch.from_numpy(rows).cuda()
+    mu64 = mu[rt].double().cpu().numpy()
+    x64 = x[rt].double().cpu().numpy()
+    o = O_fl.chain_logprob(mu64, x64, sigma_k=sig.cpu().numpy())
+    es = (0.5 * o["z"] ** 2 + np.abs(np.log(sig.cpu().numpy().astype(np.float64)))[None, :, None] + 1.0).sum(axis=(1, 2))
+    H.assert_close_rel(logp[rt].cpu().numpy(), o["logp"], 2e-7, es, "logp (sampled)")
+    p = O_ppo.ppo_loss(o["logp"], lb[rt].double().cpu().numpy(), adv[rt].double().cpu().numpy(),
+                       np.ones(256, bool), np.zeros(256, int), n_tok=float(R))
+    ok = ~p["near_tie"]
+    sens = np.abs(adv[rt].double().cpu().numpy()) * p["ratio"]
+    H.assert_close_rel(g[rt].cpu().numpy()[ok], p["grad"][ok], 1e-5, (sens * 2e-7 * es / R / 1e-5)[ok] + 1e-12, "g")
+    gr = O_fl.chain_grads(mu64, x64, g[rt].double().cpu().numpy(), sigma_k=sig.cpu().numpy())
+    bits = dmu[rt].view(torch.int16).cpu().numpy().astype(np.int32) & 0xFFFF
+    H.assert_bf16_ulp(bits, gr["dmu"], 1)
+    # statistics = fp64 sums of the per-step outputs
+    s = st.cpu().numpy()
+    assert s[11] == R and s[18] == R
+    assert abs(s[14] - logp.double().sum().item()) <= 1e-6 * logp.double().abs().sum().item()
+
+
+def test_fullsize_batcher_oft_gather():
+    """NEXT-3 at OFT observation size with 1,024 envs: 16 rounds of 64-request offers in a
+    random order and firing polls; every batch is the FIFO block and its bytes the slots'."""
+    import paper_2602_05765_b200 as P
+    from oracle import batcher as O_b
+    E, ob, B = 1024, synth.OBS_BYTES_OFT, 64
+    q = P.BatchQueue.allocate(E, ob)
+    g0 = torch.Generator(device="cuda").manual_seed(8)
+    q.obs.copy_(torch.randint(0, 256, (E, ob), generator=g0, device="cuda", dtype=torch.uint8))
+    ws = P.workspace(1)
+    cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+    out_env = torch.empty(B, dtype=torch.int32, device="cuda")
+    out_time = torch.empty(B, dtype=torch.int64, device="cuda")
+    out_n = torch.empty(1, dtype=torch.int32, device="cuda")
+    out_obs = torch.empty(B, ob, dtype=torch.uint8, device="cuda")
+    bt = O_b.Batcher(E)
+    order = np.random.default_rng(9).permutation(E)
+    for k in range(16):
+        env = order[k * B:(k + 1) * B].astype(np.int32)
+        now = 10 * k
+        P.rlvla_batch_offer(q, torch.from_numpy(env).cuda(), torch.full((B,), now, dtype=torch.int64, device="cuda"),
+                            now, cnt, ws=ws)
+        bt.offer(env, [now] * B, now)
+        P.rlvla_batch_poll(q, now, B, 5, out_env, out_time, out_n, out_obs=out_obs, ws=ws)
+        exp = bt.poll(now, B, 5)
+        assert int(out_n.item()) == len(exp) == B
+        assert out_env.cpu().tolist() == [e for e, _ in exp]
+        assert torch.equal(out_obs, q.obs[out_env.long()])
+    assert cnt.cpu().tolist() == bt.counters.tolist()
