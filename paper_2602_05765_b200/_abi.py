@@ -101,6 +101,7 @@ _SIGS = {
     "rlvla_comm_unique_id": (c_int32, [c_void_p]),
     "rlvla_comm_init": (c_int32, [c_void_p, c_int32, c_int32, POINTER(c_void_p)]),
     "rlvla_comm_destroy": (c_int32, [c_void_p]),
+    "rlvla_comm_p2p_enabled": (c_int32, [c_void_p]),
     "rlvla_status_string": (ctypes.c_char_p, [c_int32]),
     "rlvla_abi_version": (c_int32, []),
     "rlvla_nccl_version": (c_int32, []),

@@ -322,6 +322,11 @@ class Comm:
         _check(lib().rlvla_comm_init(uid2, n, rank, ctypes.byref(h)), "rlvla_comm_init", True)
         return cls(h, n, rank)
 
+    @property
+    def p2p(self) -> bool:
+        """Loss statistics reduced in-kernel over NVLink peer memory (else NCCL)."""
+        return bool(self.handle) and bool(lib().rlvla_comm_p2p_enabled(self.handle))
+
     def destroy(self):
         if self.handle:
             lib().rlvla_comm_destroy(self.handle)

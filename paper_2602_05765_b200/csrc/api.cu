@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 #include <mutex>
 
 #include "internal.cuh"
@@ -14,6 +15,11 @@ struct rlvla_comm_s {
   ncclComm_t comm;
   int nranks;
   int rank;
+  // in-kernel NVLink reduction (P2PDesc): own mailbox, peers' mailboxes mapped by CUDA IPC
+  bool p2p = false;
+  uint8_t* mbox = nullptr;
+  uint8_t* peer[rlvla::kP2PMaxRanks] = {};
+  unsigned long long* seq = nullptr;
 };
 
 namespace rlvla {
@@ -93,6 +99,19 @@ rlvla_status check_ppo_args(const rlvla_ppo_args* f) {
   if (!(f->ent_coef == f->ent_coef) || !(f->kl_coef == f->kl_coef)) return RLVLA_ERR_INVALID_ARG;
   return RLVLA_OK;
 }
+
+// the in-kernel reduction descriptor for a call that reduces its loss statistics over `c`
+P2PDesc p2p_desc(rlvla_comm c, int ch) {
+  P2PDesc d;
+  if (!c || !c->p2p || c->nranks <= 1) return d;
+  d.nranks = c->nranks;
+  d.rank = c->rank;
+  d.ch = ch;
+  for (int r = 0; r < c->nranks; ++r) d.mbox[r] = c->peer[r];
+  d.seq = c->seq;
+  return d;
+}
+bool uses_p2p(rlvla_comm c) { return c && c->p2p && c->nranks > 1; }
 
 rlvla_status allreduce_stats(double* p, int n, rlvla_comm c, cudaStream_t s) {
   if (!c || c->nranks <= 1) return RLVLA_OK;
@@ -243,11 +262,13 @@ RLVLA_API rlvla_status rlvla_logprob_fwd_bwd(const rlvla_logits* x, const int32_
   a.dlogits = dlogits;
   a.stats = grad_logp ? nullptr : stats;
   if (workspace) a.ws = carve(workspace);
+  const bool p2p = a.stats && uses_p2p(comm);
+  if (p2p) a.ws.p2p = p2p_desc(comm, P2P_CH_LOSS);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   rlvla_status st = cuda_status(launch_logprob(a, s));
   if (st != RLVLA_OK) return st;
   if (a.stats) {
-    st = allreduce_stats(stats + RLVLA_STAT_LOSS, RLVLA_STAT_DENOM - RLVLA_STAT_LOSS, comm, s);
+    if (!p2p) st = allreduce_stats(stats + RLVLA_STAT_LOSS, RLVLA_STAT_DENOM - RLVLA_STAT_LOSS, comm, s);
     if (st != RLVLA_OK) return st;
     return sync_check_stats(stats, RLVLA_STAT_N_BAD_TOK, s);
   }
@@ -277,11 +298,14 @@ RLVLA_API rlvla_status rlvla_ppo_loss(const float* logp, int64_t rows, const int
   a.loss_tok = loss_tok;
   a.stats = stats;
   if (workspace) a.ws = carve(workspace);
+  // token-level path: in-kernel NVLink reduction; the chunk-level path keeps NCCL
+  const bool p2p = stats && f->ratio_level == 0 && uses_p2p(comm);
+  if (p2p) a.ws.p2p = p2p_desc(comm, P2P_CH_LOSS);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   st = cuda_status(launch_ppo_loss(a, s));
   if (st != RLVLA_OK) return st;
   if (stats) {
-    st = allreduce_stats(stats + RLVLA_STAT_LOSS, RLVLA_STAT_DENOM - RLVLA_STAT_LOSS, comm, s);
+    if (!p2p) st = allreduce_stats(stats + RLVLA_STAT_LOSS, RLVLA_STAT_DENOM - RLVLA_STAT_LOSS, comm, s);
     if (st != RLVLA_OK) return st;
     return sync_check_stats(stats, RLVLA_STAT_N_BAD_TOK, s);
   }
@@ -416,10 +440,12 @@ RLVLA_API rlvla_status rlvla_flow_logprob(const rlvla_gauss_chain* c, float* log
   a.dlog_std = dlog_std;
   a.stats = grad_logp ? nullptr : stats;
   if (workspace) a.ws = carve(workspace);
+  const bool p2p = a.stats && uses_p2p(comm);
+  if (p2p) a.ws.p2p = p2p_desc(comm, P2P_CH_LOSS);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   rlvla_status st = cuda_status(launch_flow(a, s));
   if (st != RLVLA_OK || !a.stats) return st;
-  st = allreduce_stats(stats + RLVLA_STAT_LOSS, RLVLA_STAT_DENOM - RLVLA_STAT_LOSS, comm, s);
+  if (!p2p) st = allreduce_stats(stats + RLVLA_STAT_LOSS, RLVLA_STAT_DENOM - RLVLA_STAT_LOSS, comm, s);
   if (st != RLVLA_OK) return st;
   if (sync_check_enabled()) return sync_check_stats(stats, RLVLA_STAT_N_BAD_TOK, s);
   return RLVLA_OK;
@@ -433,6 +459,69 @@ RLVLA_API rlvla_status rlvla_comm_unique_id(void* out) {
   return RLVLA_OK;
 }
 
+namespace {
+// Mailboxes for the in-kernel NVLink reduction: each rank allocates one, the CUDA IPC
+// handles are allgathered over the new NCCL communicator and opened (peer mappings).
+// RLVLA_P2P=0 disables it; any failure leaves the communicator on NCCL collectives.
+void setup_p2p(rlvla_comm c) {
+  const char* env = std::getenv("RLVLA_P2P");
+  if (c->nranks <= 1 || c->nranks > kP2PMaxRanks || (env && env[0] == '0')) return;
+  bool ok = cudaMalloc(&c->mbox, kP2PMboxBytes) == cudaSuccess &&
+            cudaMemset(c->mbox, 0, kP2PMboxBytes) == cudaSuccess &&
+            cudaMalloc(&c->seq, kP2PChannels * sizeof(unsigned long long)) == cudaSuccess &&
+            cudaMemset(c->seq, 0, kP2PChannels * sizeof(unsigned long long)) == cudaSuccess;
+  cudaIpcMemHandle_t mine{};
+  ok = ok && cudaIpcGetMemHandle(&mine, c->mbox) == cudaSuccess;
+  void* dev = nullptr;
+  ok = ok && cudaMalloc(&dev, sizeof(cudaIpcMemHandle_t) * size_t(c->nranks + 1)) == cudaSuccess;
+  std::vector<cudaIpcMemHandle_t> all(size_t(c->nranks));
+  if (ok) {
+    uint8_t* d = static_cast<uint8_t*>(dev);
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    ok = cudaMemcpy(d + size_t(c->nranks) * hb, &mine, hb, cudaMemcpyHostToDevice) == cudaSuccess &&
+         ncclAllGather(d + size_t(c->nranks) * hb, d, hb, ncclChar, c->comm, nullptr) == ncclSuccess &&
+         cudaDeviceSynchronize() == cudaSuccess &&
+         cudaMemcpy(all.data(), d, hb * size_t(c->nranks), cudaMemcpyDeviceToHost) == cudaSuccess;
+  }
+  if (dev) cudaFree(dev);
+  int opened = 0;
+  for (int r = 0; ok && r < c->nranks; ++r) {
+    if (r == c->rank) {
+      c->peer[r] = c->mbox;
+      continue;
+    }
+    void* p = nullptr;
+    ok = cudaIpcOpenMemHandle(&p, all[size_t(r)], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+    c->peer[r] = static_cast<uint8_t*>(p);
+    opened += ok;
+  }
+  // every rank must agree: a rank that failed to map makes all of them use NCCL
+  int flag = ok ? 1 : 0;
+  int* dflag = nullptr;
+  if (cudaMalloc(&dflag, sizeof(int)) == cudaSuccess) {
+    cudaMemcpy(dflag, &flag, sizeof(int), cudaMemcpyHostToDevice);
+    if (ncclAllReduce(dflag, dflag, 1, ncclInt, ncclMin, c->comm, nullptr) == ncclSuccess &&
+        cudaDeviceSynchronize() == cudaSuccess)
+      cudaMemcpy(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost);
+    else
+      flag = 0;
+    cudaFree(dflag);
+  } else {
+    flag = 0;
+  }
+  (void)cudaGetLastError();
+  c->p2p = flag == 1;
+  if (!c->p2p) {
+    for (int r = 0; r < c->nranks; ++r)
+      if (r != c->rank && c->peer[r]) cudaIpcCloseMemHandle(c->peer[r]);
+    for (auto& q : c->peer) q = nullptr;
+    (void)opened;
+  }
+}
+}  // namespace
+
+RLVLA_API int32_t rlvla_comm_p2p_enabled(rlvla_comm c) { return (c && c->p2p) ? 1 : 0; }
+
 RLVLA_API rlvla_status rlvla_comm_init(const void* id, int32_t nranks, int32_t rank,
                                        rlvla_comm* out) {
   if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks) return RLVLA_ERR_INVALID_ARG;
@@ -445,12 +534,19 @@ RLVLA_API rlvla_status rlvla_comm_init(const void* id, int32_t nranks, int32_t r
     delete c;
     return RLVLA_ERR_NCCL;
   }
+  setup_p2p(c);  // best effort: without it the collectives stay on NCCL
   *out = c;
   return RLVLA_OK;
 }
 
 RLVLA_API rlvla_status rlvla_comm_destroy(rlvla_comm c) {
   if (!c) return RLVLA_OK;
+  if (c->p2p) {
+    for (int r = 0; r < c->nranks; ++r)
+      if (r != c->rank && c->peer[r]) cudaIpcCloseMemHandle(c->peer[r]);
+  }
+  if (c->mbox) cudaFree(c->mbox);
+  if (c->seq) cudaFree(c->seq);
   ncclResult_t r = ncclCommDestroy(c->comm);
   delete c;
   return r == ncclSuccess ? RLVLA_OK : RLVLA_ERR_NCCL;

@@ -190,9 +190,11 @@ __device__ __forceinline__ double loss_denominator(double denom, const double* a
 
 // CTA partials (12 slots) -> workspace; last CTA writes stats[6..18]
 //   LOSS = (sum m L - ent_coef sum m H) / N, PG_LOSS = sum m L_pg / N, the rest raw sums.
+// With p2p (nranks > 1) the last CTA also reduces slots 6..17 over the ranks in-kernel.
 __device__ __forceinline__ void finish_loss_stats(const double* cta_acc, double* stats,
                                                   double* partials, unsigned* ctrl, double N,
-                                                  int accumulate, float ent_coef) {
+                                                  int accumulate, float ent_coef,
+                                                  const P2PDesc* p2p = nullptr) {
   if (threadIdx.x < kLossSlots)
     partials[size_t(blockIdx.x) * RLVLA_NSTATS + threadIdx.x] = cta_acc[threadIdx.x];
   __shared__ double tot[kLossSlots];
@@ -203,8 +205,11 @@ __device__ __forceinline__ void finish_loss_stats(const double* cta_acc, double*
       if (threadIdx.x == 0) v = (v - double(ent_coef) * tot[3]) * invN;
       if (threadIdx.x == 11) v *= invN;
       if (accumulate) v += stats[RLVLA_STAT_LOSS + threadIdx.x];
-      stats[RLVLA_STAT_LOSS + threadIdx.x] = v;
+      tot[threadIdx.x] = v;
     }
+    __syncthreads();
+    if (p2p && p2p->nranks > 1) p2p_allreduce(tot, kLossSlots, *p2p);
+    if (threadIdx.x < kLossSlots) stats[RLVLA_STAT_LOSS + threadIdx.x] = tot[threadIdx.x];
     if (threadIdx.x == 0) stats[RLVLA_STAT_DENOM] = N;
   }
 }

@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(
   }
   __syncthreads();
   finish_loss_stats(cta, a.stats, a.ws.partials, a.ws.ctrl + CTRL_FLOW, Nden,
-                    MODE == 1 ? a.f.accumulate : 0, MODE == 1 ? a.f.ent_coef : 0.f);
+                    MODE == 1 ? a.f.accumulate : 0, MODE == 1 ? a.f.ent_coef : 0.f, &a.ws.p2p);
 }
 
 size_t flow_smem(int n) { return size_t((n + 3) & ~3) * 4 + size_t(kFlowWarps) * 2 * kTile * kPad * 4; }

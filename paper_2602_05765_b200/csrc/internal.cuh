@@ -21,14 +21,41 @@ enum { CTRL_SCATTER = 0, CTRL_ADV = 1, CTRL_LOGPROB = 2, CTRL_PPO = 3, CTRL_ADV2
        CTRL_BOFFER = 6, CTRL_BPOLL = 7, CTRL_FLOW = 8 };
 // ctrl words 32..35 hold two doubles of per-call scratch (chunk-ratio and value-loss 1/N)
 
+// ------------------------------------------------------------------------------------
+// In-kernel cross-rank reduction over NVLink peer memory (SURVEY §8(e) "Phase 4"): the
+// last CTA of a statistics kernel pushes its slots into every rank's mailbox (P2P stores,
+// CUDA IPC-mapped), raises a release flag there, waits for every rank's flag in its own
+// mailbox and sums the ranks in fixed order — the compute step and its collective in ONE
+// kernel, no NCCL launch. Mailbox per rank: kP2PChannels channels of
+//   data[2 parity][kP2PMaxRanks][kP2PSlots] f64, flags[2 parity][kP2PMaxRanks] u64
+// A call's sequence number s (a per-rank device counter per channel, identical on every
+// rank because calls are made in the same order) selects parity s & 1: a rank can be at
+// most one call ahead of any other on a channel, so two buffers suffice.
+constexpr int kP2PMaxRanks = 8;
+constexpr int kP2PSlots = 32;
+constexpr int kP2PChannels = 4;
+enum { P2P_CH_LOSS = 0 };
+constexpr size_t kP2PChanData = size_t(2) * kP2PMaxRanks * kP2PSlots * sizeof(double);
+constexpr size_t kP2PChanBytes = kP2PChanData + size_t(2) * kP2PMaxRanks * sizeof(unsigned long long);
+constexpr size_t kP2PMboxBytes = kP2PChannels * kP2PChanBytes;
+
+struct P2PDesc {
+  int nranks = 0;  // 0 or 1: no exchange
+  int rank = 0;
+  int ch = 0;
+  uint8_t* mbox[kP2PMaxRanks] = {};  // every rank's mailbox mapped here (mbox[rank]: own)
+  unsigned long long* seq = nullptr;  // own per-channel call counters
+};
+
 struct Workspace {
   unsigned* ctrl;      // [64]
   double* partials;    // [kMaxPartialBlocks][16]
   float* r_global;     // [n_env_global] (GRPO returns)
+  P2PDesc p2p;         // set by the API when the call reduces over ranks in-kernel
 };
 
 inline Workspace carve(void* ws) {
-  Workspace w;
+  Workspace w{};
   uint8_t* b = static_cast<uint8_t*>(ws);
   w.ctrl = reinterpret_cast<unsigned*>(b);
   w.partials = reinterpret_cast<double*>(b + kCtrlBytes);
@@ -218,6 +245,59 @@ __device__ __forceinline__ bool last_block_reduce(unsigned* ctrl_word, const dou
   __syncthreads();
   if (threadIdx.x == 0) *ctrl_word = 0u;  // leave the workspace reusable
   return true;
+}
+
+// Sum vals[0..n) (SMEM, n <= kP2PSlots) over the ranks of d, in place; called by every
+// thread of ONE CTA (the last of its grid). See P2PDesc.
+__device__ __forceinline__ void p2p_allreduce(double* vals, int n, const P2PDesc& d) {
+  __shared__ unsigned long long s_seq;
+  if (threadIdx.x == 0) {
+    s_seq = d.seq[d.ch] + 1ull;
+    d.seq[d.ch] = s_seq;
+  }
+  __syncthreads();
+  const unsigned long long sq = s_seq;
+  const int par = int(sq & 1ull);
+  const size_t dofs = size_t(d.ch) * kP2PChanBytes;
+  // 1) my slots into every rank's mailbox (NVLink stores to peers)
+  for (int i = threadIdx.x; i < d.nranks * n; i += blockDim.x) {
+    const int pr = i / n, k = i - pr * n;
+    double* dst = reinterpret_cast<double*>(d.mbox[pr] + dofs) + (par * kP2PMaxRanks + d.rank) * kP2PSlots + k;
+    asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(dst), "d"(vals[k]) : "memory");
+  }
+  __threadfence_system();
+  __syncthreads();
+  // 2) raise my flag at every rank (release: the data above is visible first)
+  if (threadIdx.x < d.nranks) {
+    unsigned long long* f = reinterpret_cast<unsigned long long*>(d.mbox[threadIdx.x] + dofs + kP2PChanData) +
+                            par * kP2PMaxRanks + d.rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(sq) : "memory");
+  }
+  // 3) wait for every rank's flag in my mailbox
+  if (threadIdx.x < d.nranks) {
+    const unsigned long long* f =
+        reinterpret_cast<const unsigned long long*>(d.mbox[d.rank] + dofs + kP2PChanData) + par * kP2PMaxRanks +
+        threadIdx.x;
+    unsigned long long v;
+    uint32_t it = 0;
+    do {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+      if (++it > (1u << 30)) __trap();  // a rank never arrived: fail loudly, do not hang
+    } while (v != sq);
+  }
+  __syncthreads();
+  // 4) fixed rank order sum
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const double* src = reinterpret_cast<const double*>(d.mbox[d.rank] + dofs) + par * kP2PMaxRanks * kP2PSlots + k;
+    double acc = 0.0;
+    for (int r = 0; r < d.nranks; ++r) {
+      double v;
+      asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(src + r * kP2PSlots) : "memory");
+      acc += v;
+    }
+    vals[k] = acc;
+  }
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------------------------

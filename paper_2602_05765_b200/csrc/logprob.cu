@@ -67,6 +67,7 @@ struct Lp {
   double* stats;
   double* partials;
   unsigned* ctrl;
+  P2PDesc p2p;
 };
 
 template <typename T>
@@ -690,7 +691,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     __syncthreads();
     if (tid < kLossSlots) gacc[tid] += gacc[16 + tid];  // fixed order: group 0 then group 1
     __syncthreads();
-    finish_loss_stats(gacc, p.stats, p.partials, p.ctrl, Nden, p.accumulate, pc.ent_coef);
+    finish_loss_stats(gacc, p.stats, p.partials, p.ctrl, Nden, p.accumulate, pc.ent_coef, &p.p2p);
   }
 }
 
@@ -813,7 +814,7 @@ __global__ void __launch_bounds__(256) lp_warp_kernel(Lp p) {
       cta[threadIdx.x] = s;
     }
     __syncthreads();
-    finish_loss_stats(cta, p.stats, p.partials, p.ctrl, Nden, p.accumulate, pc.ent_coef);
+    finish_loss_stats(cta, p.stats, p.partials, p.ctrl, Nden, p.accumulate, pc.ent_coef, &p.p2p);
   }
 }
 
@@ -906,7 +907,7 @@ __global__ void __launch_bounds__(256) lp_generic_kernel(Lp p) {
   }
   if (want_stats) {
     __syncthreads();
-    finish_loss_stats(sacc, p.stats, p.partials, p.ctrl, Nden, p.accumulate, pc.ent_coef);
+    finish_loss_stats(sacc, p.stats, p.partials, p.ctrl, Nden, p.accumulate, pc.ent_coef, &p.p2p);
   }
 }
 
@@ -923,6 +924,7 @@ Lp make_lp(const LpArgs& a) {
   p.g_in = a.grad_logp;
   p.dx = a.dlogits;
   p.stats = a.stats;
+  p.p2p = a.ws.p2p;
   p.partials = a.ws.partials;
   p.ctrl = a.ws.ctrl + CTRL_LOGPROB;
   if (a.fused) {

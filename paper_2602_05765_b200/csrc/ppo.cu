@@ -24,7 +24,7 @@ __device__ __forceinline__ void block_finish(double* acc, int nslot, const PpoAr
     cta[threadIdx.x] = s;
   }
   __syncthreads();
-  finish_loss_stats(cta, a.stats, a.ws.partials, ctrl, N, a.f.accumulate, ent_coef);
+  finish_loss_stats(cta, a.stats, a.ws.partials, ctrl, N, a.f.accumulate, ent_coef, &a.ws.p2p);
 }
 
 __global__ void __launch_bounds__(256) ppo_loss_kernel(PpoArgs a, PpoConst pc0) {

@@ -17,7 +17,7 @@ def L():
 
 def test_exports_every_header_symbol(L):
     names = A.header_functions()
-    assert len(names) == 15
+    assert len(names) == 16
     for n in names:
         assert hasattr(L, n), n
     assert set(names) == set(A._SIGS)

@@ -168,7 +168,8 @@ def main():
     assert s5[11] == rf[1].item() and s5[18] == Nf
     dist.barrier()
     if rank == 0:
-        print(f"MGPU PARITY OK world={world} nccl={P.rlvla_nccl_version()}", flush=True)
+        print(f"MGPU PARITY OK world={world} nccl={P.rlvla_nccl_version()} "
+              f"in-kernel-p2p={comm.p2p}", flush=True)
     comm.destroy()
     dist.destroy_process_group()
 
