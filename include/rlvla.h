@@ -392,14 +392,14 @@ RLVLA_API rlvla_status rlvla_comm_unique_id(void* out_id_128_bytes);
 RLVLA_API rlvla_status rlvla_comm_init(const void* nccl_unique_id, int32_t nranks, int32_t rank,
                              rlvla_comm* out);
 RLVLA_API rlvla_status rlvla_comm_destroy(rlvla_comm c);
-/* 1 when the communicator reduces the loss statistics (slots 6..17 of rlvla_logprob_fwd_bwd,
- * token-level rlvla_ppo_loss and rlvla_flow_logprob) INSIDE the computing kernel over
- * NVLink peer memory (every rank's mailbox mapped through CUDA IPC at rlvla_comm_init; the
- * kernel's last CTA pushes its slots to all ranks and sums them in rank order), 0 when
- * those calls use an NCCL allreduce after the kernel. RLVLA_P2P=0 at init forces NCCL.
- * Calls with one communicator must be stream-ordered and made in the same order on every
- * rank (as for NCCL). C1/C2 (rlvla_advantages), the value loss and the chunk-ratio path
- * always use NCCL. */
+/* 1 when the communicator reduces statistics INSIDE the computing kernel over NVLink peer
+ * memory (every rank's mailbox mapped through CUDA IPC at rlvla_comm_init; the kernel's last
+ * CTA pushes its slots to all ranks and sums them in rank order): C1 and the GRPO returns
+ * allgather C2 in rlvla_advantages (n_env_global <= 32768), C3 in rlvla_logprob_fwd_bwd,
+ * token-level rlvla_ppo_loss and rlvla_flow_logprob. 0 when those calls use NCCL
+ * collectives after the kernel. RLVLA_P2P=0 at init forces NCCL. Calls with one communicator
+ * must be stream-ordered and made in the same order on every rank (as for NCCL). The value
+ * loss and the chunk-ratio path always use NCCL. */
 RLVLA_API int32_t rlvla_comm_p2p_enabled(rlvla_comm c);
 
 RLVLA_API const char* rlvla_status_string(rlvla_status s);

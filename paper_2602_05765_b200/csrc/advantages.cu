@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(256) gae_scan_kernel(AdvArgs a) {
   }
   __shared__ double tot[6];
   if (last_block_reduce(a.ws.ctrl + CTRL_ADV, a.ws.partials, 6, tot)) {
+    if (a.ws.p2p.nranks > 1) p2p_exchange(tot, 6, a.ws.p2p);  // C1 in-kernel (NVLink)
     if (threadIdx.x < 6) a.stats[threadIdx.x] = tot[threadIdx.x];
   }
 }
@@ -207,6 +208,10 @@ __global__ void __launch_bounds__(256) grpo_returns_kernel(AdvArgs a) {
   }
   __shared__ double tot[6];
   if (last_block_reduce(a.ws.ctrl + CTRL_ADV, a.ws.partials, 6, tot)) {
+    // C1 + C2 in-kernel (NVLink): statistics summed, every rank's returns gathered
+    if (a.ws.p2p.nranks > 1)
+      p2p_exchange(tot, 6, a.ws.p2p, a.ws.r_global + a.p.env_offset, a.p.env_offset, E, a.ws.r_global,
+                   a.p.n_env_global);
     if (threadIdx.x < 6) a.stats[threadIdx.x] = tot[threadIdx.x];
   }
 }

@@ -206,9 +206,12 @@ RLVLA_API rlvla_status rlvla_advantages(const rlvla_traj_buffer* buf, const floa
   if (!device_ready()) return RLVLA_ERR_CUDA;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   AdvArgs a{*buf, last_value, *p, adv, ret, stats, carve(workspace)};
+  // C1 (+ C2) inside the pass-1 kernel over NVLink when the mailbox can hold the returns
+  const bool p2p = uses_p2p(comm) && p->n_env_global <= kP2PMaxEnvGlobal;
+  if (p2p) a.ws.p2p = p2p_desc(comm, P2P_CH_ADV);
   st = cuda_status(launch_adv_pass1(a, s));
   if (st != RLVLA_OK) return st;
-  if (comm && comm->nranks > 1) {
+  if (!p2p && comm && comm->nranks > 1) {
     if (ncclGroupStart() != ncclSuccess) return RLVLA_ERR_NCCL;
     ncclResult_t r1 = ncclAllReduce(stats, stats, 6, ncclDouble, ncclSum, comm->comm, s);
     ncclResult_t r2 = ncclSuccess;

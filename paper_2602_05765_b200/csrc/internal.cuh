@@ -34,10 +34,13 @@ enum { CTRL_SCATTER = 0, CTRL_ADV = 1, CTRL_LOGPROB = 2, CTRL_PPO = 3, CTRL_ADV2
 constexpr int kP2PMaxRanks = 8;
 constexpr int kP2PSlots = 32;
 constexpr int kP2PChannels = 4;
-enum { P2P_CH_LOSS = 0 };
+enum { P2P_CH_LOSS = 0, P2P_CH_ADV = 1 };
 constexpr size_t kP2PChanData = size_t(2) * kP2PMaxRanks * kP2PSlots * sizeof(double);
 constexpr size_t kP2PChanBytes = kP2PChanData + size_t(2) * kP2PMaxRanks * sizeof(unsigned long long);
-constexpr size_t kP2PMboxBytes = kP2PChannels * kP2PChanBytes;
+// gather region (C2: GRPO returns of all ranks), [2 parity][kP2PMaxEnvGlobal] f32
+constexpr int kP2PMaxEnvGlobal = 32768;
+constexpr size_t kP2PGatherOffset = kP2PChannels * kP2PChanBytes;
+constexpr size_t kP2PMboxBytes = kP2PGatherOffset + size_t(2) * kP2PMaxEnvGlobal * sizeof(float);
 
 struct P2PDesc {
   int nranks = 0;  // 0 or 1: no exchange
@@ -247,9 +250,13 @@ __device__ __forceinline__ bool last_block_reduce(unsigned* ctrl_word, const dou
   return true;
 }
 
-// Sum vals[0..n) (SMEM, n <= kP2PSlots) over the ranks of d, in place; called by every
-// thread of ONE CTA (the last of its grid). See P2PDesc.
-__device__ __forceinline__ void p2p_allreduce(double* vals, int n, const P2PDesc& d) {
+// Sum vals[0..n) (SMEM, n <= kP2PSlots) over the ranks of d, in place; optionally also
+// allgather a float slice: this rank's gsrc[0..glen) lands at [goff, goff + glen) of gdst
+// [0..gtotal) on every rank (gtotal <= kP2PMaxEnvGlobal). Called by every thread of ONE CTA
+// (the last of its grid). One flag per rank covers both. See P2PDesc.
+__device__ __forceinline__ void p2p_exchange(double* vals, int n, const P2PDesc& d,
+                                             const float* gsrc = nullptr, int goff = 0, int glen = 0,
+                                             float* gdst = nullptr, int gtotal = 0) {
   __shared__ unsigned long long s_seq;
   if (threadIdx.x == 0) {
     s_seq = d.seq[d.ch] + 1ull;
@@ -259,11 +266,17 @@ __device__ __forceinline__ void p2p_allreduce(double* vals, int n, const P2PDesc
   const unsigned long long sq = s_seq;
   const int par = int(sq & 1ull);
   const size_t dofs = size_t(d.ch) * kP2PChanBytes;
-  // 1) my slots into every rank's mailbox (NVLink stores to peers)
+  const size_t gofs = kP2PGatherOffset + size_t(par) * kP2PMaxEnvGlobal * sizeof(float);
+  // 1) my slots (and my slice) into every rank's mailbox (NVLink stores to peers)
   for (int i = threadIdx.x; i < d.nranks * n; i += blockDim.x) {
     const int pr = i / n, k = i - pr * n;
     double* dst = reinterpret_cast<double*>(d.mbox[pr] + dofs) + (par * kP2PMaxRanks + d.rank) * kP2PSlots + k;
     asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(dst), "d"(vals[k]) : "memory");
+  }
+  for (int i = threadIdx.x; i < d.nranks * glen; i += blockDim.x) {
+    const int pr = i / glen, k = i - pr * glen;
+    float* dst = reinterpret_cast<float*>(d.mbox[pr] + gofs) + goff + k;
+    asm volatile("st.relaxed.sys.global.f32 [%0], %1;" ::"l"(dst), "f"(__ldcg(gsrc + k)) : "memory");
   }
   __threadfence_system();
   __syncthreads();
@@ -286,7 +299,7 @@ __device__ __forceinline__ void p2p_allreduce(double* vals, int n, const P2PDesc
     } while (v != sq);
   }
   __syncthreads();
-  // 4) fixed rank order sum
+  // 4) fixed rank order sum; the gathered slices copied out
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
     const double* src = reinterpret_cast<const double*>(d.mbox[d.rank] + dofs) + par * kP2PMaxRanks * kP2PSlots + k;
     double acc = 0.0;
@@ -297,8 +310,17 @@ __device__ __forceinline__ void p2p_allreduce(double* vals, int n, const P2PDesc
     }
     vals[k] = acc;
   }
+  for (int k = threadIdx.x; k < gtotal; k += blockDim.x) {
+    float v;
+    asm volatile("ld.relaxed.sys.global.f32 %0, [%1];"
+                 : "=f"(v)
+                 : "l"(reinterpret_cast<const float*>(d.mbox[d.rank] + gofs) + k)
+                 : "memory");
+    gdst[k] = v;
+  }
   __syncthreads();
 }
+__device__ __forceinline__ void p2p_allreduce(double* vals, int n, const P2PDesc& d) { p2p_exchange(vals, n, d); }
 
 // ------------------------------------------------------------------------------------
 // host side
