@@ -334,9 +334,11 @@ RLVLA_API rlvla_status rlvla_value_loss(const float* v_new, const float* v_old, 
   if (!device_ready()) return RLVLA_ERR_CUDA;
   ValueArgs a{v_new, v_old, ret, slot_key, version, n_steps, cur_version, max_staleness, clip_eps,
               denominator, grad_v, loss_step, stats, carve(workspace)};
+  const bool p2p = stats && uses_p2p(comm);
+  if (p2p) a.ws.p2p = p2p_desc(comm, P2P_CH_VALUE);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   rlvla_status st = cuda_status(launch_value_loss(a, s));
-  if (st != RLVLA_OK || !stats) return st;
+  if (st != RLVLA_OK || !stats || p2p) return st;
   return allreduce_stats(stats + RLVLA_STAT_VALUE_LOSS,
                          RLVLA_STAT_VALUE_DENOM - RLVLA_STAT_VALUE_LOSS, comm, s);
 }

@@ -34,7 +34,7 @@ enum { CTRL_SCATTER = 0, CTRL_ADV = 1, CTRL_LOGPROB = 2, CTRL_PPO = 3, CTRL_ADV2
 constexpr int kP2PMaxRanks = 8;
 constexpr int kP2PSlots = 32;
 constexpr int kP2PChannels = 4;
-enum { P2P_CH_LOSS = 0, P2P_CH_ADV = 1 };
+enum { P2P_CH_LOSS = 0, P2P_CH_ADV = 1, P2P_CH_VALUE = 2 };
 constexpr size_t kP2PChanData = size_t(2) * kP2PMaxRanks * kP2PSlots * sizeof(double);
 constexpr size_t kP2PChanBytes = kP2PChanData + size_t(2) * kP2PMaxRanks * sizeof(unsigned long long);
 // gather region (C2: GRPO returns of all ranks), [2 parity][kP2PMaxEnvGlobal] f32

@@ -60,16 +60,20 @@ __global__ void __launch_bounds__(256) value_loss_kernel(ValueArgs a) {
   }
   __shared__ double tot[3];
   if (last_block_reduce(a.ws.ctrl + CTRL_VALUE, a.ws.partials, 3, tot)) {
+    const double N = explicit_n ? a.denominator : tot[2];
+    const double inv = N > 0.0 ? 1.0 / N : 0.0;
+    __syncthreads();
     if (threadIdx.x == 0) {
-      const double N = explicit_n ? a.denominator : tot[2];
-      const double inv = N > 0.0 ? 1.0 / N : 0.0;
-      if (a.stats) {
-        a.stats[RLVLA_STAT_VALUE_LOSS] = tot[0] * inv;
-        a.stats[RLVLA_STAT_N_VALUE_CLIPPED] = tot[1];
-        a.stats[RLVLA_STAT_N_VALUE_STEPS] = tot[2];
-        a.stats[RLVLA_STAT_VALUE_DENOM] = N;
-      }
       *value_scratch(a) = inv;
+      tot[0] *= inv;  // this rank's share of the loss, as the NCCL path reduces it
+    }
+    __syncthreads();
+    if (a.stats && a.ws.p2p.nranks > 1) p2p_exchange(tot, 3, a.ws.p2p);  // in-kernel (NVLink)
+    if (threadIdx.x == 0 && a.stats) {
+      a.stats[RLVLA_STAT_VALUE_LOSS] = tot[0];
+      a.stats[RLVLA_STAT_N_VALUE_CLIPPED] = tot[1];
+      a.stats[RLVLA_STAT_N_VALUE_STEPS] = tot[2];
+      a.stats[RLVLA_STAT_VALUE_DENOM] = N;
     }
   }
 }
