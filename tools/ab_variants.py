@@ -12,12 +12,11 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
-    "fused_neginf": ("RLVLA_NEGINF_FUSED=1",),
-
+    "scatter_nopdl": ("RLVLA_SCATTER_PDL=0",),
 }
 # name -> git revision whose csrc/ + include/ are built as one more variant
 # (the ABI only grew at the end of its structs, so today's binding drives older libraries)
-REVISIONS = {"prev": "HEAD"}  # e.g. {"pre_next2": "6cd809f"}
+REVISIONS = {}  # e.g. {"pre_next2": "6cd809f"}
 
 
 def build_revision(name, rev):
@@ -61,7 +60,7 @@ def build():
 
 
 def run(mode="fused", rounds=3):
-    """mode: fused | fwd | bwd (tools/prof_fused.py) or batcher (tools/prof_batcher.py)."""
+    """mode: fused | fwd | bwd (tools/prof_fused.py), batcher, scatter or flow (tools/prof_*.py)."""
     res = {}
     for _ in range(rounds):
         for name in list(VARIANTS) + list(REVISIONS):
@@ -70,6 +69,8 @@ def run(mode="fused", rounds=3):
             env = dict(os.environ, RLVLA_LIB=os.path.join(VAR, f"{name}.so"))
             if mode == "batcher":
                 cmd = [sys.executable, os.path.join(ROOT, "tools", "prof_batcher.py"), "--iters", "30"]
+            elif mode == "scatter":
+                cmd = [sys.executable, os.path.join(ROOT, "tools", "prof_scatter.py")]
             elif mode == "flow":
                 cmd = [sys.executable, os.path.join(ROOT, "tools", "prof_flow.py"), "--rows", "196608"]
             else:
@@ -85,6 +86,8 @@ def run(mode="fused", rounds=3):
                 res.setdefault(name, []).append((round(d["poll_us_min"], 2), round(d["poll_us_median"], 2)))
             elif mode == "flow":
                 res.setdefault(name, []).append((round(d["us_min"], 1), round(d["us_median"], 1)))
+            elif mode == "scatter":
+                res.setdefault(name, []).append(round(d["us_per_call"], 2))
             else:
                 res.setdefault(name, []).append((round(d["ms_min"], 3), round(d["ms_avg"], 3)))
     print(json.dumps(res))
