@@ -197,3 +197,93 @@ def test_fullsize_batcher_oft_gather():
         assert out_env.cpu().tolist() == [e for e, _ in exp]
         assert torch.equal(out_obs, q.obs[out_env.long()])
     assert cnt.cpu().tolist() == bt.counters.tolist()
+
+
+@pytest.mark.parametrize("name", ["libero10_long", "maniskill_ppo_gae", "grpo_span"])
+def test_fullsize_microbatched_configs(name):
+    """BASELINE.json configs 2-4 at full size in the launch configuration bench.py times on
+    one GPU (e.g. LIBERO-10: 256 envs x 128 decision steps, 1.8 M logit rows): every
+    arrival-chunk scatter, the advantages over the full buffer (GAE + global whitening, or
+    GRPO with interleaved groups; compared with the oracle in full), then the fused S3+S4
+    call on micro-batches of <= 131,072 rows — the first and the ragged last one — with
+    logits generated per micro-batch, sampled rows against the oracle."""
+    import paper_2602_05765_b200 as P
+    cfg = synth.CONFIGS[name]
+    E, T, A, V = cfg.n_env, cfg.t_steps, cfg.a_tok, cfg.vocab
+    traj = synth.make_trajectories(cfg)
+    rec = synth.make_records(traj, 0, E)
+    rows_of = synth.record_rows(rec, cfg, E)                       # [M, A] logit rows
+    env_rows = T * A
+    mb_envs = 131072 // env_rows
+    mbs = [(e0, min(E, e0 + mb_envs)) for e0 in range(0, E, mb_envs)]
+    tested = [mbs[0], mbs[-1]]
+    rng = np.random.default_rng(11)
+    # behaviour log-probs: oracle logp + noise for the sampled rows' records, synthetic elsewhere
+    lb = (-3.0 + 0.5 * rng.standard_normal(rec.behav_noise.shape)).astype(np.float32)
+    samples = {}
+    for e0, e1 in tested:
+        lo, hi = e0 * env_rows, e1 * env_rows
+        pick = rng.choice(np.arange(lo, hi), 96, replace=False)
+        samples[(e0, e1)] = np.sort(pick)
+        x = synth.gen_logits(cfg, traj, e0, e1, device="cuda")[torch.from_numpy(pick - lo).cuda()].double().cpu().numpy()
+        for k, r in enumerate(pick):
+            m, a = np.argwhere(rows_of == r)[0] if (rows_of == r).any() else (None, None)
+            if m is None:
+                continue
+            f = O_lp.log_softmax_gather(x[k:k + 1], rec.tokens[m, a:a + 1])
+            if np.isfinite(f["logp"][0]):
+                lb[m, a] = np.float32(f["logp"][0] + rec.behav_noise[m, a])
+    case = H.Case(cfg, traj, 0, E, rec, lb, None)
+    gbuf, gcnt = H.gpu_scatter(case)
+    obuf, ocnt = H.oracle_scatter(case)
+    assert gcnt.cpu().numpy().tolist() == ocnt.tolist()
+    ws = P.workspace(E)
+    stats = torch.zeros(24, dtype=torch.float64, device="cuda")
+    adv = torch.zeros(E, T, device="cuda")
+    ret = torch.zeros(E, T, device="cuda")
+    if cfg.adv_mode == "grpo":
+        prm = P.adv_params("grpo", group_id=torch.from_numpy(traj.group_id).cuda(),
+                           group_size=cfg.group_size, n_env_global=E, cur_version=synth.CUR_VERSION)
+        P.rlvla_advantages(gbuf, None, prm, adv, ret, stats, ws)
+        oadv = H.oracle_advantages(case, obuf, "grpo")
+        H.assert_close_rel(adv.cpu().numpy(), oadv["adv"], 1e-5, 1e-3, "adv (grpo)")
+    else:
+        prm = P.adv_params("gae", gamma=0.99, lam=0.95, whiten=cfg.whiten, n_env_global=E,
+                           cur_version=synth.CUR_VERSION)
+        P.rlvla_advantages(gbuf, torch.from_numpy(traj.last_value).cuda(), prm, adv, ret, stats, ws)
+        oadv = H.oracle_advantages(case, obuf, "gae", whiten=cfg.whiten)
+        H.assert_close_rel(adv.cpu().numpy(), oadv["adv"], 1e-5, 1.0, "adv (gae)")
+    assert stats[3].item() == oadv["counts"]["n_tok"]
+    a32 = adv.cpu().numpy().astype(np.float64)
+    tv = O_path.token_view(obuf, a32, A, synth.CUR_VERSION)
+    N = stats[3].item()
+    for e0, e1 in tested:
+        lo, hi = e0 * env_rows, e1 * env_rows
+        xmb = synth.gen_logits(cfg, traj, e0, e1, device="cuda")
+        n = hi - lo
+        logp = torch.empty(n, device="cuda")
+        g = torch.empty(n, device="cuda")
+        dx = torch.empty_like(xmb)
+        st = torch.zeros(24, dtype=torch.float64, device="cuda")
+        s0, s1 = lo // A, hi // A
+        fa = P.ppo_args(logp_behav=gbuf.logp_behav.view(-1)[lo:hi], adv=adv.view(-1)[s0:s1],
+                        version=gbuf.version.view(-1)[s0:s1], slot_key=gbuf.slot_key.view(-1)[s0:s1],
+                        a_tok=A, cur_version=synth.CUR_VERSION, adv_stats=stats, out_grad_logp=g)
+        P.rlvla_logprob_fwd_bwd(xmb, gbuf.tokens.view(-1)[lo:hi], logp=logp, fused=fa, dlogits=dx,
+                                stats=st, ws=ws)
+        torch.cuda.synchronize()
+        rows = samples[(e0, e1)]
+        x = xmb[torch.from_numpy(rows - lo).cuda()].double().cpu().numpy()
+        ref = O_path.loss_and_grad(x, tv, n_tok=N, rows=rows)
+        H.assert_close_rel(logp.cpu().numpy()[rows - lo], ref["fwd"]["logp"], 1e-5, 1.0, "logp")
+        nt = ref["ppo"]["near_tie"]
+        H.assert_close_rel(g.cpu().numpy()[rows - lo][~nt], ref["ppo"]["grad"][~nt], 1e-5, 1e-9, "grad")
+        bits = dx[torch.from_numpy(rows - lo).cuda()].view(torch.int16).cpu().numpy().astype(np.int32) & 0xFFFF
+        H.assert_bf16_ulp(bits[~nt], ref["dx"][~nt], 1)
+        # the call's token count = the oracle's masked tokens of this micro-batch
+        allr = np.arange(lo, hi)
+        base = tv["valid"][allr] & (tv["target"][allr] >= 0) & (tv["lag"][allr] >= 0) & (tv["lag"][allr] <= 1)
+        assert st.cpu().numpy()[11] == base.sum() - 0  # no non-finite logits in these envs
+        assert st.cpu().numpy()[18] == N
+        del xmb, dx
+        torch.cuda.empty_cache()
