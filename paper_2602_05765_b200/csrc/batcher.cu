@@ -16,20 +16,18 @@
 //                       observations are gathered into the batch, the concatenated rows
 //                       split evenly over one CTA per SM (128-bit loads/stores: one read
 //                       + one write of b * obs_bytes, HBM-bound); the last CTA pops the
-//                       ring.
+//                       ring. (Measured and rejected: TMA bulk copies through an SMEM ring,
+//                       256-thread CTAs, 8 or 16 loads in flight per thread — equal or slower.)
 #include "internal.cuh"
 
 namespace rlvla {
 namespace {
 
-#ifndef RLVLA_POLL_TMA
-#define RLVLA_POLL_TMA 0  // 1: gather through TMA bulk copies (SMEM ring) instead of SIMT loads
-#endif
 #ifndef RLVLA_POLL_THREADS
 #define RLVLA_POLL_THREADS 1024  // threads per poll CTA; the grid keeps 1024 threads per SM
 #endif
 constexpr int kPollThreads = RLVLA_POLL_THREADS;
-constexpr int kPollCtasPerSm = RLVLA_POLL_TMA ? 1 : 1024 / kPollThreads;
+constexpr int kPollCtasPerSm = 1024 / kPollThreads;
 
 #ifndef RLVLA_COPY_DEPTH
 #define RLVLA_COPY_DEPTH 4  // 16-byte loads in flight per thread (A/B: 4 < 8 < 16 in time)
@@ -66,63 +64,6 @@ __device__ __forceinline__ void grid_copy_rows(int nrows, int64_t ob16, Dst dst_
     cta_copy16(dst_row(int(row)) + off, src_row(int(row)) + off, end - x);
     x = end;
   }
-}
-
-// TMA variant of grid_copy_rows: one thread streams the CTA's word range through a ring of
-// kTmaStages SMEM stages (bulk load -> mbarrier -> bulk store), pieces never crossing a row
-constexpr int kTmaStages = 4;
-constexpr int64_t kTmaPiece16 = 3072;  // 48 KB pieces
-template <typename Dst, typename Src>
-__device__ __forceinline__ void grid_copy_rows_tma(int nrows, int64_t ob16, Dst dst_row, Src src_row,
-                                                   uint8_t* stage_mem, uint64_t* bars) {
-  const int64_t total = int64_t(nrows) * ob16;
-  const int64_t per = (total + gridDim.x - 1) / gridDim.x;
-  const int64_t lo = int64_t(blockIdx.x) * per;
-  const int64_t hi = lo + per < total ? lo + per : total;
-  if (threadIdx.x != 0 || lo >= hi) return;
-  const uint64_t pol = policy_evict_first();
-  // piece j: words [x_j, x_j + n_j) of the range; generated in order
-  auto next = [&](int64_t& x, int64_t& n) {
-    const int64_t row = x / ob16;
-    const int64_t row_end = (row + 1) * ob16 < hi ? (row + 1) * ob16 : hi;
-    n = row_end - x < kTmaPiece16 ? row_end - x : kTmaPiece16;
-  };
-  int64_t xs[kTmaStages], ns[kTmaStages];
-  int64_t x = lo;
-  int issued = 0;
-  for (; issued < kTmaStages && x < hi; ++issued) {
-    int64_t n;
-    next(x, n);
-    xs[issued] = x;
-    ns[issued] = n;
-    const int64_t row = x / ob16;
-    mbar_arrive_expect_tx(&bars[issued], uint32_t(n * 16));
-    bulk_g2s(stage_mem + size_t(issued) * kTmaPiece16 * 16, src_row(int(row)) + (x - row * ob16),
-             uint32_t(n * 16), &bars[issued], pol);
-    x += n;
-  }
-  for (int j = 0; j < issued; ++j) {
-    const int st = j % kTmaStages;
-    mbar_wait(&bars[st], uint32_t(j / kTmaStages) & 1u);
-    const int64_t row = xs[st] / ob16;
-    bulk_s2g(dst_row(int(row)) + (xs[st] - row * ob16), stage_mem + size_t(st) * kTmaPiece16 * 16,
-             uint32_t(ns[st] * 16));
-    bulk_commit();
-    if (x < hi) {  // refill this stage once the store has read it
-      bulk_wait_read_all();
-      int64_t n;
-      next(x, n);
-      xs[st] = x;
-      ns[st] = n;
-      const int64_t r2 = x / ob16;
-      mbar_arrive_expect_tx(&bars[st], uint32_t(n * 16));
-      bulk_g2s(stage_mem + size_t(st) * kTmaPiece16 * 16, src_row(int(r2)) + (x - r2 * ob16),
-               uint32_t(n * 16), &bars[st], pol);
-      x += n;
-      ++issued;
-    }
-  }
-  bulk_wait_all();
 }
 
 __device__ __forceinline__ bool cta_is_last(unsigned* ctrl_word) {
@@ -253,19 +194,7 @@ __global__ void __launch_bounds__(kPollThreads) batch_poll_kernel(BatchPollArgs 
       const int env = staged ? s_env[k] : a.q.ring_env[(head + k) % cap];
       return slots + int64_t(env) * ob16;
     };
-#if RLVLA_POLL_TMA
-    extern __shared__ __align__(128) uint8_t stage_mem[];
-    __shared__ uint64_t bars[kTmaStages];
-    if (threadIdx.x == 0) {
-      for (int i = 0; i < kTmaStages; ++i) mbar_init(&bars[i], 1);
-      fence_mbar_init();
-    }
-    __syncthreads();
-    grid_copy_rows_tma(b, ob16, dst, src, stage_mem, bars);
-    __syncthreads();
-#else
     grid_copy_rows(b, ob16, dst, src);
-#endif
   }
   if (blockIdx.x == 0)
     for (int k = threadIdx.x; k < b; k += blockDim.x) {
@@ -323,19 +252,7 @@ cudaError_t launch_batch_offer(const BatchOfferArgs& a, cudaStream_t s) {
 cudaError_t launch_batch_poll(const BatchPollArgs& a, cudaStream_t s) {
   const int64_t rows = a.b_max < a.q.n_env ? a.b_max : a.q.n_env;
   const int grid = (a.out_obs != nullptr && a.q.obs_bytes > 0) ? copy_grid(rows, a.q.obs_bytes, kPollCtasPerSm) : 1;
-#if RLVLA_POLL_TMA
-  const size_t smem = size_t(kTmaStages) * kTmaPiece16 * 16;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(batch_poll_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  return launch_pdl(batch_poll_kernel, grid, kPollThreads, a, s, smem);
-#else
   return launch_pdl(batch_poll_kernel, grid, kPollThreads, a, s);
-#endif
 }
 
 }  // namespace rlvla

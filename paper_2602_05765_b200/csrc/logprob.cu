@@ -24,12 +24,6 @@ enum { MODE_FWD = 0, MODE_FUSED = 1, MODE_BWD = 2 };
 #ifndef RLVLA_NFULL_FUSED
 #define RLVLA_NFULL_FUSED 0  // A/B: unchecked vectors cost the fused kernel 4-5% (one spill at 64 regs)
 #endif
-#ifndef RLVLA_F32X2
-#define RLVLA_F32X2 1  // 0: scalar fp32 arithmetic in the TMA kernel's passes B and C
-#endif
-#ifndef RLVLA_PACKED_CLAMP
-#define RLVLA_PACKED_CLAMP 1  // 0: clamp t per element (A/B: 1 is ~1.5% faster)
-#endif
 // (Measured and rejected: a NaN-guarded per-vector redo instead of the per-element -inf
 // clamp in the entropy partial — 4% slower, the per-vector branch costs more than it saves.)
 
@@ -104,19 +98,12 @@ struct RowGrad {
   float c;
 };
 
-#ifndef RLVLA_SPLIT_STATS
-#define RLVLA_SPLIT_STATS 1  // 0: statistics evaluated before pass C's scalars are published
-#endif
 
 // per-row results kept until they are stored (after pass C's scalars are published)
 struct RowOut {
   float logp, lse;
   PpoRowIn in;
   PpoMid mid;
-#if !RLVLA_SPLIT_STATS
-  RowStats rs;
-  float lt;
-#endif
 };
 
 // critical part: the row's g and c (and what the statistics need later)
@@ -139,16 +126,7 @@ __device__ __forceinline__ RowGrad eval_row(const Lp& p, const PpoConst& pc, int
     o.in.valid = mt.key != 0ull;
     out.g = ppo_grad(pc, o.in, o.mid);
     out.c = o.mid.m ? pc.ent_coef * pc.invN : 0.f;
-#if !RLVLA_SPLIT_STATS
-    ppo_stats(pc, o.in, o.mid, o.rs, &o.lt);
-#endif
   }
-#if !RLVLA_SPLIT_STATS
-  else {
-    fwd_row_stats(o.in, o.rs);
-    o.lt = 0.f;
-  }
-#endif
   return out;
 }
 
@@ -156,15 +134,10 @@ __device__ __forceinline__ RowGrad eval_row(const Lp& p, const PpoConst& pc, int
 template <int MODE>
 __device__ __forceinline__ void write_row(const Lp& p, const PpoConst& pc, int64_t r,
                                           const RowGrad& rg, const RowOut& o, double* acc) {
-#if RLVLA_SPLIT_STATS
   RowStats rs;
   float lt = 0.f;
   if (MODE == MODE_FUSED) ppo_stats(pc, o.in, o.mid, rs, &lt);
   else fwd_row_stats(o.in, rs);
-#else
-  const RowStats& rs = o.rs;
-  const float lt = o.lt;
-#endif
   p.logp[r] = o.logp;
   if (p.lse_out) p.lse_out[r] = o.lse;
   if (MODE == MODE_FUSED) {
@@ -213,37 +186,18 @@ __device__ __forceinline__ double resolve_pc(const Lp& p, PpoConst& pc) {
   return N;
 }
 
-// ln S and logp = (x_a - M) - ln S. The direct form has an absolute error of a few fp32
-// ulps of ln S, which is all any consumer needs (the ratio e^{logp - logp_behav} and every
-// gradient term carry it as a relative error). The log1p form keeps relative accuracy for
-// |logp| << 1 (a saturated row: logp ~ -1e-24 instead of 0): S = e_a (1 + S_rest/e_a), so
-// logp = -log1p(S_rest/e_a) and ln S = t_a ln2 + log1p(S_rest/e_a). A/B (tools/ab_variants.py):
-// the branch costs 0.7% of the fused kernel's time, so the product keeps the direct form.
-#ifndef RLVLA_LSE_MODE
-#define RLVLA_LSE_MODE 0  // 0: direct form; 1: log1p form whenever e_a > 2^-100; 2: when S_rest < e_a
-#endif
+// ln S and logp = (x_a - M) - ln S in the direct form: an absolute error of a few fp32 ulps
+// of ln S, which is all any consumer needs (the ratio e^{logp - logp_behav} and every
+// gradient term carry it as a relative error). (Measured and rejected: the log1p form
+// logp = -log1p(S_rest/e_a), which keeps relative accuracy for |logp| << 1, costs 0.7%.)
 struct LseParts {
   float lnS;
   float logp;
 };
-__device__ __forceinline__ LseParts lse_parts(float xa, float M, float ta, float ea, float Srest,
-                                              float Stot, bool tgt_ok) {
+__device__ __forceinline__ LseParts lse_parts(float xa, float M, float Stot) {
   LseParts o;
-#if RLVLA_LSE_MODE == 0
-  const bool use = false;
-#elif RLVLA_LSE_MODE == 1
-  const bool use = tgt_ok && ea > 7.9e-31f;
-#else
-  const bool use = tgt_ok && Srest < ea;
-#endif
-  if (use) {
-    const float l1 = log1pf(__fdividef(Srest, ea));
-    o.logp = -l1;
-    o.lnS = fmaf(ta, kLn2, l1);
-  } else {
-    o.lnS = __logf(Stot);
-    o.logp = (xa - M) - o.lnS;
-  }
+  o.lnS = __logf(Stot);
+  o.logp = (xa - M) - o.lnS;
   return o;
 }
 
@@ -449,7 +403,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
       // The target column is excluded from the pass-B sums (so that 1 - p_a = S_rest / S
       // keeps full relative precision near saturation) by overwriting it with -inf in the
       // stage once the max has seen it; only its owner thread reads that vector again.
-      if ((kNegInfTarget || !RLVLA_F32X2) && owner) {
+      if (kNegInfTarget && owner) {
         uint16_t* hx = reinterpret_cast<uint16_t*>(row);
         *gxa = bf_lo(uint32_t(hx[a]));
         hx[a] = 0xFF80u;
@@ -458,7 +412,6 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
       mws = (mw == -INFINITY) ? 0.f : mw;
       const float nmL = -mws * L2E;
       // ---- pass B: e = 2^(t), t = (x - m_warp) log2e; s = sum e, et = sum e t ------
-#if RLVLA_F32X2
       // packed fp32x2 arithmetic (FFMA2 / FADD2): two columns per instruction; the
       // thread's sums stay in two lanes of a float2 until the end of the row
       float2 s2 = make_float2(0.f, 0.f), et2 = make_float2(0.f, 0.f);
@@ -506,52 +459,6 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
         }
       }
       float s = s2.x + s2.y, et = et2.x + et2.y;
-#else
-      float s = 0.f, et = 0.f;
-#pragma unroll
-      for (int i = 0; i < kVecPerThread; ++i) {
-        const int idx = gt + i * kGroupThreads;
-        if (i < NFULL || idx < nvec) {
-          const uint4 w = rv[idx];
-          const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
-          float e[8];
-          float vs = 0.f, vet = 0.f;
-#if RLVLA_PACKED_CLAMP
-          // -inf -> -2^100 once per bf16 pair (NaN-propagating max): e = 0 and e*t = 0 for
-          // those columns without a per-element clamp; NaN and +inf pass through unchanged
-          uint32_t c4[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) c4[q] = bmax2_nan(w4[q], kNegClampPair);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float t0 = fmaf(bf_lo(c4[q]), L2E, nmL);
-            const float t1 = fmaf(bf_hi(c4[q]), L2E, nmL);
-            e[2 * q] = ex2(t0);
-            e[2 * q + 1] = ex2(t1);
-            vs += e[2 * q] + e[2 * q + 1];
-            vet = fmaf(e[2 * q], t0, vet);
-            vet = fmaf(e[2 * q + 1], t1, vet);
-          }
-#else
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float t0 = fmaf(bf_lo(w4[q]), L2E, nmL);
-            const float t1 = fmaf(bf_hi(w4[q]), L2E, nmL);
-            e[2 * q] = ex2(t0);
-            e[2 * q + 1] = ex2(t1);
-            vs += e[2 * q] + e[2 * q + 1];
-            vet = fmaf(e[2 * q], fmaxf(t0, -256.f), vet);      // -inf column: 0 * -256
-            vet = fmaf(e[2 * q + 1], fmaxf(t1, -256.f), vet);
-          }
-#endif
-          if (keep_e)
-            rv[idx] = make_uint4(pack_bf16x2(e[0], e[1]), pack_bf16x2(e[2], e[3]),
-                                 pack_bf16x2(e[4], e[5]), pack_bf16x2(e[6], e[7]));
-          s += vs;
-          et += vet;
-        }
-      }
-#endif
       s = warp_sum(s);
       et = warp_sum(et);
       if (lane == 0) gred[gw] = make_float4(mw, s, et, 0.f);
@@ -579,7 +486,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
         const float ta = (xa - M) * L2E;
         const float ea = tgt_ok ? ex2(ta) : 0.f;
         const float Stot = Srest + ea;
-        const LseParts lp = lse_parts(xa, M, ta, ea, Srest, Stot, tgt_ok);
+        const LseParts lp = lse_parts(xa, M, Stot);
         const float lnS = lp.lnS;
         const float lse_row = M + lnS;
         const float logp = lp.logp;
@@ -640,12 +547,8 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
               // FUSED: dx = g' 2^{(m_w - M) log2e} e, e from pass B (bf16 in SMEM)
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
-#if RLVLA_F32X2
                 const float2 d = __fmul2_rn(make_float2(bf_lo(w4[q]), bf_hi(w4[q])), make_float2(kw, kw));
                 ow[q] = pack_bf16x2(d.x, d.y);
-#else
-                ow[q] = pack_bf16x2(kw * bf_lo(w4[q]), kw * bf_hi(w4[q]));
-#endif
               }
             } else {
               // from x: t = (x - M) log2e (lse in external bwd), dx = 2^t (k1 + k2 t);
@@ -653,18 +556,11 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 const uint32_t c = bmax2_nan(w4[q], kNegClampPair);
-#if RLVLA_F32X2
                 const float2 t2 = __ffma2_rn(make_float2(bf_lo(c), bf_hi(c)), make_float2(L2E, L2E),
                                              make_float2(nML, nML));
                 const float2 f2 = __ffma2_rn(make_float2(rsv.k2, rsv.k2), t2, make_float2(rsv.k1, rsv.k1));
                 const float2 d2 = __fmul2_rn(make_float2(ex2(t2.x), ex2(t2.y)), f2);
                 ow[q] = pack_bf16x2(d2.x, d2.y);
-#else
-                const float t0 = fmaf(bf_lo(c), L2E, nML);
-                const float t1 = fmaf(bf_hi(c), L2E, nML);
-                ow[q] = pack_bf16x2(ex2(t0) * fmaf(rsv.k2, t0, rsv.k1),
-                                    ex2(t1) * fmaf(rsv.k2, t1, rsv.k1));
-#endif
               }
             }
             if (idx == va) {  // the target column (0 from its -inf) takes g (1 - p_a) [+ ...]
@@ -757,7 +653,7 @@ __global__ void __launch_bounds__(256) lp_warp_kernel(Lp p) {
       const float ta = (xa - Ms) * L2E;
       ea = tgt_ok ? ex2(ta) : 0.f;
       Stot = Srest + ea;
-      const LseParts lp = lse_parts(xa, M, ta, ea, Srest, Stot, tgt_ok);
+      const LseParts lp = lse_parts(xa, M, Stot);
       lnS = lp.lnS;
       const float lse_row = M + lnS;
       logp = lp.logp;
@@ -875,7 +771,7 @@ __global__ void __launch_bounds__(256) lp_generic_kernel(Lp p) {
       const float ta = (xa - Ms) * L2E;
       ea = tgt_ok ? ex2(ta) : 0.f;
       Stot = Srest + ea;
-      const LseParts lp = lse_parts(xa, M, ta, ea, Srest, Stot, tgt_ok);
+      const LseParts lp = lse_parts(xa, M, Stot);
       lnS = lp.lnS;
       lse_row = M + lnS;
       logp = lp.logp;

@@ -12,7 +12,8 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
-    "scatter_nopdl": ("RLVLA_SCATTER_PDL=0",),
+    "fused_neginf": ("RLVLA_NEGINF_FUSED=1",),
+    "fused_unchecked": ("RLVLA_NFULL_FUSED=1",),
 }
 # name -> git revision whose csrc/ + include/ are built as one more variant
 # (the ABI only grew at the end of its structs, so today's binding drives older libraries)
