@@ -18,8 +18,10 @@
  *   - Pointers are DEVICE pointers unless marked (host). Structs passed by pointer are
  *     HOST structs whose members are device pointers.
  *   - Every call enqueues its work on `stream` (a cudaStream_t; NULL = legacy default
- *     stream) and returns without synchronising. Collectives (when `comm` != NULL) are
- *     enqueued on the same stream (NCCL), so a whole iteration is CUDA-graph capturable.
+ *     stream) and returns without synchronising. Cross-rank reductions (when `comm` !=
+ *     NULL) run inside the computing kernel over NVLink peer memory, or as NCCL collectives
+ *     on the same stream (rlvla_comm_p2p_enabled), so a whole iteration is CUDA-graph
+ *     capturable.
  *   - Ownership: the caller owns every buffer, including `workspace`. The library
  *     allocates nothing in these calls and keeps no pointer after return. Its only state
  *     is the communicator handle and a per-device property cache.
@@ -187,7 +189,7 @@ typedef struct {
  * delta_t = v_t (r_t + gamma (nt_t V_{t+1} + tr_t B_t) - V_t) with V_T = last_value[e]
  * (NULL => 0), B = boot_value; A_t = delta_t + gamma lam nt_t A_{t+1}. Computed as a warp-parallel suffix scan of the
  * affine maps A -> delta_t + c_t A (fp32, fp64 statistics).
- * stats: device double[16]; slots 0..5 written and allreduced over `comm` (C1). With
+ * stats: device double[RLVLA_NSTATS]; slots 0..5 written and reduced over `comm` (C1). With
  * GRPO and comm != NULL the per-env returns are allgathered (C2) first. */
 RLVLA_API rlvla_status rlvla_advantages(const rlvla_traj_buffer* buf, const float* last_value,
                               const rlvla_adv_params* p, float* adv, float* ret,
@@ -252,14 +254,14 @@ typedef struct {
  *   external bwd    : fused == NULL, grad_logp != NULL, lse (input!) != NULL, dlogits;
  *                     one read of x, one write of dlogits, logp not written
  *   fused PPO       : fused != NULL: one pass computing logp, the PPO epilogue g_r and
- *                     (if dlogits != NULL) dlogits; stats slots 6..15; over `comm` C3.
+ *                     (if dlogits != NULL) dlogits; stats slots 6..18; over `comm` C3.
  * target: int32[rows]; -1 => ignore (logp = 0, zero gradient row); other targets
  * outside [0, V) are counted in N_BAD_TOK and treated as ignored (R4). Non-finite
  * results (NaN/+inf logits, all -inf row, -inf target logit) give a non-finite logp,
  * are counted and masked (R5). logp: float[rows] (written except in external bwd);
  * lse: float[rows] or NULL (output in forward/fused modes). dlogits: same dtype/ld as
  * x, may alias x->ptr (each row is read completely before it is written); masked rows
- * are written as zeros. stats: NULL or device double[16]. */
+ * are written as zeros. stats: NULL or device double[RLVLA_NSTATS]. */
 RLVLA_API rlvla_status rlvla_logprob_fwd_bwd(const rlvla_logits* x, const int32_t* target, float* logp,
                                    float* lse, const float* grad_logp,
                                    const rlvla_ppo_args* fused, void* dlogits, double* stats,
@@ -270,7 +272,7 @@ RLVLA_API rlvla_status rlvla_logprob_fwd_bwd(const rlvla_logits* x, const int32_
  * another forward). target: int32[rows] or NULL (all usable); rows whose target is
  * outside [0, ...) or whose logp is non-finite are masked (no vocab bound is known
  * here, so only target < 0 / non-finite are checked). grad_logp: float[rows] output
- * (required); loss_tok: float[rows] or NULL. stats slots 6..15 (entropy slot = 0). */
+ * (required); loss_tok: float[rows] or NULL. stats slots 6..18 (entropy slot = 0). */
 RLVLA_API rlvla_status rlvla_ppo_loss(const float* logp, int64_t rows, const int32_t* target,
                             const rlvla_ppo_args* a, float* grad_logp, float* loss_tok,
                             double* stats, void* workspace, size_t ws_bytes, rlvla_comm comm,

@@ -1,6 +1,7 @@
 // api.cu — the extern "C" boundary (include/rlvla.h): argument validation, dispatch to the
-// kernels, and the NCCL collectives C1 (advantage statistics allreduce), C2 (GRPO returns
-// allgather) and C3 (loss statistics allreduce), all enqueued on the caller's stream.
+// kernels, and the cross-rank exchanges C1 (advantage statistics), C2 (GRPO returns) and C3
+// (loss statistics): inside the kernels over IPC-mapped NVLink mailboxes (set up here at
+// communicator init), else NCCL collectives on the caller's stream.
 #include <nccl.h>
 
 #include <cstdio>

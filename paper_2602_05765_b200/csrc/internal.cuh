@@ -52,7 +52,7 @@ struct P2PDesc {
 
 struct Workspace {
   unsigned* ctrl;      // [64]
-  double* partials;    // [kMaxPartialBlocks][16]
+  double* partials;    // [kMaxPartialBlocks][RLVLA_NSTATS]
   float* r_global;     // [n_env_global] (GRPO returns)
   P2PDesc p2p;         // set by the API when the call reduces over ranks in-kernel
 };
