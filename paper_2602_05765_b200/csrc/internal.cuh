@@ -282,7 +282,9 @@ __device__ __forceinline__ void p2p_exchange(double* vals, int n, const P2PDesc&
     uint32_t it = 0;
     do {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
-      if (++it > (1u << 30)) __trap();  // a rank never arrived: fail loudly, do not hang
+      // a rank never arrived (crashed, or calls out of order): fail loudly after ~2^27 polls
+      // (about a minute) instead of hanging the GPU
+      if (++it > (1u << 27)) __trap();
     } while (v != sq);
   }
   __syncthreads();
