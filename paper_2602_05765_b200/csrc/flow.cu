@@ -79,7 +79,7 @@ struct RowMeta4 {
 
 // One row's lane partials: q = sum z^2 and ls = sum ln sigma (learned) over the lane's
 // elements. Row pointers are formed once, indices stay 32-bit.
-template <typename T, bool VEC>
+template <typename T, bool VEC, int NQ>
 __device__ __forceinline__ void row_partials(const FlowArgs& a, const float* s_isig, int64_t base,
                                              int n, bool learned, int lane, float& q, float& ls) {
   const T* mu = static_cast<const T*>(a.c.mu) + base;
@@ -89,23 +89,31 @@ __device__ __forceinline__ void row_partials(const FlowArgs& a, const float* s_i
   ls = 0.f;
   if (VEC) {
     float2 q2 = make_float2(0.f, 0.f);
-    for (int j = 4 * lane; j < n; j += 128) {
-      const float4 m = ld_mu4<T>(mu, j);
-      const float4 xv = *reinterpret_cast<const float4*>(x + j);
-      float4 iv;
-      if (learned) {
-        const float4 l = *reinterpret_cast<const float4*>(lsd + j);
-        iv = make_float4(__expf(-l.x), __expf(-l.y), __expf(-l.z), __expf(-l.w));
-        ls += (l.x + l.y) + (l.z + l.w);
-      } else {
-        iv = *reinterpret_cast<const float4*>(s_isig + j);
+    // NQ > 0: the row length is a compile-time constant (the paper's K D shapes), so the
+    // loop unrolls into predicated copies with immediate offsets
+    constexpr int kIters = NQ > 0 ? (NQ + 31) / 32 : 1;
+    const int nq = NQ > 0 ? NQ : (n >> 2);
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+      for (int gi = lane + 32 * it; gi < nq; gi += (NQ > 0 ? nq : 32)) {
+        const int j = 4 * gi;
+        const float4 m = ld_mu4<T>(mu, j);
+        const float4 xv = *reinterpret_cast<const float4*>(x + j);
+        float4 iv;
+        if (learned) {
+          const float4 l = *reinterpret_cast<const float4*>(lsd + j);
+          iv = make_float4(__expf(-l.x), __expf(-l.y), __expf(-l.z), __expf(-l.w));
+          ls += (l.x + l.y) + (l.z + l.w);
+        } else {
+          iv = *reinterpret_cast<const float4*>(s_isig + j);
+        }
+        // packed fp32x2 (FADD2 / FMUL2 / FFMA2): two elements per instruction
+        const float2 za = __fmul2_rn(__fadd2_rn(make_float2(xv.x, xv.y), make_float2(-m.x, -m.y)),
+                                     make_float2(iv.x, iv.y));
+        const float2 zb = __fmul2_rn(__fadd2_rn(make_float2(xv.z, xv.w), make_float2(-m.z, -m.w)),
+                                     make_float2(iv.z, iv.w));
+        q2 = __ffma2_rn(za, za, __ffma2_rn(zb, zb, q2));
       }
-      // packed fp32x2 (FADD2 / FMUL2 / FFMA2): two elements per instruction
-      const float2 za = __fmul2_rn(__fadd2_rn(make_float2(xv.x, xv.y), make_float2(-m.x, -m.y)),
-                                   make_float2(iv.x, iv.y));
-      const float2 zb = __fmul2_rn(__fadd2_rn(make_float2(xv.z, xv.w), make_float2(-m.z, -m.w)),
-                                   make_float2(iv.z, iv.w));
-      q2 = __ffma2_rn(za, za, __ffma2_rn(zb, zb, q2));
     }
     q = q2.x + q2.y;
   } else {
@@ -126,7 +134,7 @@ __device__ __forceinline__ void row_partials(const FlowArgs& a, const float* s_i
 }
 
 // dmu = g z / sigma, dln sigma = g (z^2 - 1) - c for one row (exact zeros when g = c = 0)
-template <typename T, bool VEC>
+template <typename T, bool VEC, int NQ>
 __device__ __forceinline__ void row_backward(const FlowArgs& a, const float* s_isig, int64_t base,
                                              int n, bool learned, int lane, float g, float c) {
   const bool active = g != 0.f || c != 0.f;
@@ -136,7 +144,12 @@ __device__ __forceinline__ void row_backward(const FlowArgs& a, const float* s_i
   T* dmu = a.dmu ? static_cast<T*>(a.dmu) + base : nullptr;
   float* dls = a.dlog_std ? a.dlog_std + base : nullptr;
   if (VEC) {
-    for (int j = 4 * lane; j < n; j += 128) {
+    constexpr int kIters = NQ > 0 ? (NQ + 31) / 32 : 1;
+    const int nq = NQ > 0 ? NQ : (n >> 2);
+#pragma unroll
+    for (int it = 0; it < kIters; ++it)
+    for (int gi = lane + 32 * it; gi < nq; gi += (NQ > 0 ? nq : 32)) {
+      const int j = 4 * gi;
       float4 dm = make_float4(0.f, 0.f, 0.f, 0.f), dl = dm;
       if (active) {
         const float4 m = ld_mu4<T>(mu, j);
@@ -187,7 +200,7 @@ __device__ __forceinline__ void row_backward(const FlowArgs& a, const float* s_i
 #ifndef RLVLA_FLOW_MINB
 #define RLVLA_FLOW_MINB 4  // resident CTAs per SM the register budget is sized for
 #endif
-template <typename T, int MODE, bool VEC>
+template <typename T, int MODE, bool VEC, int NQ>
 __global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(FlowArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int K = a.c.n_steps, D = a.c.dim, n = K * D;
@@ -255,7 +268,7 @@ __global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(
 #pragma unroll 2
       for (int t = 0; t < nt; ++t) {  // pass 1: lane partials of each row -> SMEM
         float q, ls;
-        row_partials<T, VEC>(a, s_isig, (r0 + t) * n, n, learned, lane, q, ls);
+        row_partials<T, VEC, NQ>(a, s_isig, (r0 + t) * n, n, learned, lane, q, ls);
         pq[t * kPad + lane] = q;
         if (learned) pl[t * kPad + lane] = ls;
       }
@@ -303,7 +316,7 @@ __global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(
       for (int t = 0; t < nt; ++t) {  // pass 2 (the rows were just read: L1/L2 hits)
         const float gt = __shfl_sync(0xffffffffu, g, t);
         const float ct = __shfl_sync(0xffffffffu, c, t);
-        row_backward<T, VEC>(a, s_isig, (r0 + t) * n, n, learned, lane, gt, ct);
+        row_backward<T, VEC, NQ>(a, s_isig, (r0 + t) * n, n, learned, lane, gt, ct);
       }
     }
   }
@@ -328,19 +341,19 @@ __global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(
 size_t flow_smem(int n) { return size_t((n + 3) & ~3) * 4 + size_t(kFlowWarps) * 2 * kTile * kPad * 4; }
 
 // grid = all resident CTAs (occupancy of the instantiation), fewer for small problems
-template <typename T, int MODE, bool VEC>
+template <typename T, int MODE, bool VEC, int NQ>
 cudaError_t launch_m(const FlowArgs& a, cudaStream_t s) {
   const int n = a.c.n_steps * a.c.dim;
   const size_t smem = flow_smem(n);
   static size_t attr = 0;
   if (smem > 48 * 1024 && attr < smem) {
-    cudaError_t e = cudaFuncSetAttribute(flow_kernel<T, MODE, VEC>,
+    cudaError_t e = cudaFuncSetAttribute(flow_kernel<T, MODE, VEC, NQ>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     attr = smem;
   }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel<T, MODE, VEC>,
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel<T, MODE, VEC, NQ>,
                                                                 kFlowWarps * 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
@@ -348,15 +361,25 @@ cudaError_t launch_m(const FlowArgs& a, cudaStream_t s) {
   int64_t grid = (tiles + kFlowWarps - 1) / kFlowWarps;
   const int64_t cap = int64_t(device_info().sm_count) * per_sm;
   if (grid > cap) grid = cap;
-  flow_kernel<T, MODE, VEC><<<int(grid), kFlowWarps * 32, smem, s>>>(a);
+  flow_kernel<T, MODE, VEC, NQ><<<int(grid), kFlowWarps * 32, smem, s>>>(a);
   return cudaGetLastError();
 }
 
+template <typename T, bool VEC, int NQ>
+cudaError_t launch_q(const FlowArgs& a, cudaStream_t s) {
+  if (a.grad_logp) return launch_m<T, 2, VEC, NQ>(a, s);
+  if (a.fused) return launch_m<T, 1, VEC, NQ>(a, s);
+  return launch_m<T, 0, VEC, NQ>(a, s);
+}
+
+// the paper's shapes (Table 2: K = 4 denoising steps, chunk 10 or 5 x 7 DoF) get a compile-time
+// row length; every other 4-aligned shape the runtime one
 template <typename T, bool VEC>
 cudaError_t launch_v(const FlowArgs& a, cudaStream_t s) {
-  if (a.grad_logp) return launch_m<T, 2, VEC>(a, s);
-  if (a.fused) return launch_m<T, 1, VEC>(a, s);
-  return launch_m<T, 0, VEC>(a, s);
+  const int n = a.c.n_steps * a.c.dim;
+  if (VEC && n == 280) return launch_q<T, VEC, 70>(a, s);
+  if (VEC && n == 140) return launch_q<T, VEC, 35>(a, s);
+  return launch_q<T, VEC, 0>(a, s);
 }
 
 template <typename T>

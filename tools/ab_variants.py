@@ -12,12 +12,10 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
-    "fused_neginf": ("RLVLA_NEGINF_FUSED=1",),
-    "fused_unchecked": ("RLVLA_NFULL_FUSED=1",),
 }
 # name -> git revision whose csrc/ + include/ are built as one more variant
 # (the ABI only grew at the end of its structs, so today's binding drives older libraries)
-REVISIONS = {}  # e.g. {"pre_next2": "6cd809f"}
+REVISIONS = {"prev": "HEAD"}  # e.g. {"pre_next2": "6cd809f"}
 
 
 def build_revision(name, rev):
