@@ -80,11 +80,12 @@ struct RowMeta4 {
 // One row's lane partials: q = sum z^2 and ls = sum ln sigma (learned) over the lane's
 // elements. Row pointers are formed once, indices stay 32-bit.
 template <typename T, bool VEC, int NQ>
-__device__ __forceinline__ void row_partials(const FlowArgs& a, const float* s_isig, int64_t base,
-                                             int n, bool learned, int lane, float& q, float& ls) {
-  const T* mu = static_cast<const T*>(a.c.mu) + base;
-  const float* x = a.c.x + base;
-  const float* lsd = learned ? a.c.log_std + base : nullptr;
+__device__ __forceinline__ void row_partials(const T* mu0, const float* x0, const float* ls0,
+                                             const float* s_isig, int64_t base, int n, bool learned,
+                                             int lane, float& q, float& ls) {
+  const T* mu = mu0 + base;
+  const float* x = x0 + base;
+  const float* lsd = learned ? ls0 + base : nullptr;
   q = 0.f;
   ls = 0.f;
   if (VEC) {
@@ -135,14 +136,15 @@ __device__ __forceinline__ void row_partials(const FlowArgs& a, const float* s_i
 
 // dmu = g z / sigma, dln sigma = g (z^2 - 1) - c for one row (exact zeros when g = c = 0)
 template <typename T, bool VEC, int NQ>
-__device__ __forceinline__ void row_backward(const FlowArgs& a, const float* s_isig, int64_t base,
-                                             int n, bool learned, int lane, float g, float c) {
+__device__ __forceinline__ void row_backward(const T* mu0, const float* x0, const float* ls0, T* dmu0,
+                                             float* dls0, const float* s_isig, int64_t base, int n,
+                                             bool learned, int lane, float g, float c) {
   const bool active = g != 0.f || c != 0.f;
-  const T* mu = static_cast<const T*>(a.c.mu) + base;
-  const float* x = a.c.x + base;
-  const float* lsd = learned ? a.c.log_std + base : nullptr;
-  T* dmu = a.dmu ? static_cast<T*>(a.dmu) + base : nullptr;
-  float* dls = a.dlog_std ? a.dlog_std + base : nullptr;
+  const T* mu = mu0 + base;
+  const float* x = x0 + base;
+  const float* lsd = learned ? ls0 + base : nullptr;
+  T* dmu = dmu0 ? dmu0 + base : nullptr;
+  float* dls = dls0 ? dls0 + base : nullptr;
   if (VEC) {
     constexpr int kIters = NQ > 0 ? (NQ + 31) / 32 : 1;
     const int nq = NQ > 0 ? NQ : (n >> 2);
@@ -203,9 +205,15 @@ __device__ __forceinline__ void row_backward(const FlowArgs& a, const float* s_i
 template <typename T, int MODE, bool VEC, int NQ>
 __global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(FlowArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int K = a.c.n_steps, D = a.c.dim, n = K * D;
+  const int K = a.c.n_steps, D = a.c.dim, n = NQ > 0 ? 4 * NQ : K * D;
   const bool learned = a.c.log_std != nullptr;
   const bool want_stats = a.stats != nullptr && MODE != 2;
+  // the row arrays in registers once (not re-read from the parameter bank per row)
+  const T* const mu0 = static_cast<const T*>(a.c.mu);
+  const float* const x0 = a.c.x;
+  const float* const ls0 = a.c.log_std;
+  T* const dmu0 = static_cast<T*>(a.dmu);
+  float* const dls0 = a.dlog_std;
   extern __shared__ __align__(16) float dsm[];
   float* s_isig = dsm;                                        // [n] (sigma schedule)
   float* pq = dsm + ((n + 3) & ~3) + warp * 2 * kTile * kPad;  // [kTile][kPad] per warp
@@ -268,7 +276,7 @@ __global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(
 #pragma unroll 2
       for (int t = 0; t < nt; ++t) {  // pass 1: lane partials of each row -> SMEM
         float q, ls;
-        row_partials<T, VEC, NQ>(a, s_isig, (r0 + t) * n, n, learned, lane, q, ls);
+        row_partials<T, VEC, NQ>(mu0, x0, ls0, s_isig, (r0 + t) * n, n, learned, lane, q, ls);
         pq[t * kPad + lane] = q;
         if (learned) pl[t * kPad + lane] = ls;
       }
@@ -316,7 +324,7 @@ __global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(
       for (int t = 0; t < nt; ++t) {  // pass 2 (the rows were just read: L1/L2 hits)
         const float gt = __shfl_sync(0xffffffffu, g, t);
         const float ct = __shfl_sync(0xffffffffu, c, t);
-        row_backward<T, VEC, NQ>(a, s_isig, (r0 + t) * n, n, learned, lane, gt, ct);
+        row_backward<T, VEC, NQ>(mu0, x0, ls0, dmu0, dls0, s_isig, (r0 + t) * n, n, learned, lane, gt, ct);
       }
     }
   }
