@@ -308,13 +308,25 @@ typedef struct {
   int32_t n_env;        /* envs served by this queue (= ring capacity; an env waits for its */
                         /* action, so it has at most one pending request)                  */
   int64_t obs_bytes;    /* observation payload per env in bytes, multiple of 16 (0 = none) */
-  uint8_t* obs;         /* [n_env * obs_bytes] observation slots, 16-byte aligned          */
+  uint8_t* obs;         /* observation rows (16-byte aligned), see obs_fifo               */
   int32_t* ring_env;    /* [n_env] FIFO ring: env of each pending request                  */
   int64_t* ring_time;   /* [n_env] FIFO ring: its enqueue time                             */
   uint8_t* pending;     /* [n_env] 1 while the env has a request in the ring               */
-  int64_t* state;       /* int64[4]: head, tail (request counts since creation), anchor,   */
-                        /* number of batches emitted. Zero-filled at creation; owned by    */
-                        /* the device (the library never reads it on the host)             */
+  int64_t* state;       /* int64[8]: head, tail (request counts since creation), anchor,   */
+                        /* number of batches emitted, first obs row of the last batch      */
+                        /* (obs_fifo), 3 reserved. Zero-filled at creation; owned by the   */
+                        /* device (the library never reads it on the host)                 */
+  int32_t obs_fifo;     /* 0: obs = [n_env] slots indexed by env (the env side may write   */
+                        /*    its slot in place; a poll GATHERS the batch into out_obs)    */
+                        /* 1: obs = [n_env + max_batch] rows indexed by FIFO position: the */
+                        /*    offer copies obs_src into its request's row, so a batch is   */
+                        /*    already contiguous: rows [state[4], state[4] + b) of obs     */
+                        /*    (a wrap copies at most b - 1 rows past n_env). Half the      */
+                        /*    bytes of mode 0 per request; offers must carry obs_src. The  */
+                        /*    rows stay valid until later accepted offers reuse their ring */
+                        /*    positions: consume the batch in stream order before offering */
+                        /*    n_env - (requests still pending) more.                       */
+  int32_t max_batch;    /* obs_fifo: the largest b_max any poll will use (<= n_env)        */
 } rlvla_batch_queue;
 
 /* Batcher counters: int64[4], ADDED to by rlvla_batch_offer (caller zeroes). */
@@ -335,7 +347,8 @@ RLVLA_API rlvla_status rlvla_batch_offer(const rlvla_batch_queue* q, const int32
                                          const void* obs_src, int64_t* counters,
                                          void* workspace, size_t ws_bytes, void* stream);
 
-/* poll (Eq. (1)): with p = pending count, the queue fires iff p >= b_max or
+/* poll (Eq. (1)) — with obs_fifo = 1 out_obs may be NULL (the batch is rows
+ * [state[4], state[4] + b) of q->obs); otherwise: with p = pending count, the queue fires iff p >= b_max or
  * (p >= 1 and now - anchor >= t_max); then b = min(p, b_max) oldest requests leave in FIFO
  * order: out_env[i], out_time[i] (device [b_max]) and, if out_obs != NULL, their
  * observations gathered into out_obs[i * obs_bytes ...] (device [b_max * obs_bytes],

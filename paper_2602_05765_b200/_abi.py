@@ -68,7 +68,7 @@ BCNT_OOB, BCNT_FUTURE, BCNT_DUP, BCNT_ACCEPTED = range(4)
 class c_batch_queue(ctypes.Structure):
     _fields_ = [("n_env", c_int32), ("obs_bytes", c_int64), ("obs", c_void_p),
                 ("ring_env", c_void_p), ("ring_time", c_void_p), ("pending", c_void_p),
-                ("state", c_void_p)]
+                ("state", c_void_p), ("obs_fifo", c_int32), ("max_batch", c_int32)]
 
 
 class c_gauss_chain(ctypes.Structure):

@@ -215,22 +215,31 @@ class BatchQueue:
     """rlvla_batch_queue: one rollout worker's Eq. (1) request queue (NEXT-3)."""
     n_env: int
     obs_bytes: int
-    obs: torch.Tensor | None   # u8 [n_env, obs_bytes] observation slots
+    obs: torch.Tensor | None   # u8 [n_env (+ max_batch), obs_bytes] observation rows
     ring_env: torch.Tensor     # i32 [n_env]
     ring_time: torch.Tensor    # i64 [n_env]
     pending: torch.Tensor      # u8 [n_env]
-    state: torch.Tensor        # i64 [4] head, tail, anchor, batches
+    state: torch.Tensor        # i64 [8] head, tail, anchor, batches, batch row, reserved
+    obs_fifo: int = 0
+    max_batch: int = 0
 
     @classmethod
-    def allocate(cls, n_env, obs_bytes=0, device="cuda"):
+    def allocate(cls, n_env, obs_bytes=0, device="cuda", obs_fifo=False, max_batch=0):
         z = lambda *s, dt: torch.zeros(*s, dtype=dt, device=device)  # noqa: E731
-        obs = z(n_env, obs_bytes, dt=torch.uint8) if obs_bytes > 0 else None
+        rows = n_env + (max_batch if obs_fifo else 0)
+        obs = z(rows, obs_bytes, dt=torch.uint8) if obs_bytes > 0 else None
         return cls(n_env, obs_bytes, obs, z(n_env, dt=torch.int32), z(n_env, dt=torch.int64),
-                   z(n_env, dt=torch.uint8), z(4, dt=torch.int64))
+                   z(n_env, dt=torch.uint8), z(8, dt=torch.int64), int(obs_fifo), int(max_batch))
+
+    def batch_rows(self, b: int) -> torch.Tensor:
+        """obs_fifo: the last emitted batch (b rows), a view into obs (no copy)."""
+        r0 = int(self.state[4].item())
+        return self.obs[r0:r0 + b]
 
     def c(self) -> A.c_batch_queue:
         return A.c_batch_queue(self.n_env, self.obs_bytes, _ptr(self.obs), _ptr(self.ring_env),
-                               _ptr(self.ring_time), _ptr(self.pending), _ptr(self.state))
+                               _ptr(self.ring_time), _ptr(self.pending), _ptr(self.state),
+                               self.obs_fifo, self.max_batch)
 
 
 def rlvla_batch_offer(q: BatchQueue, env_id, enqueue_time, now: int, counters, *, obs_src=None,

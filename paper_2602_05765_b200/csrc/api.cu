@@ -354,6 +354,8 @@ rlvla_status check_queue(const rlvla_batch_queue* q) {
     return RLVLA_ERR_INVALID_ARG;
   if (misaligned(q->state, 8) || misaligned(q->ring_time, 8) || misaligned(q->ring_env, 4))
     return RLVLA_ERR_INVALID_ARG;
+  if (q->obs_fifo != 0 && q->obs_fifo != 1) return RLVLA_ERR_INVALID_ARG;
+  if (q->obs_fifo && (q->max_batch < 1 || q->max_batch > q->n_env)) return RLVLA_ERR_INVALID_ARG;
   return RLVLA_OK;
 }
 
@@ -375,6 +377,7 @@ RLVLA_API rlvla_status rlvla_batch_offer(const rlvla_batch_queue* q, const int32
     return RLVLA_ERR_INVALID_ARG;
   if (n > 0 && (!env_id || !enqueue_time || misaligned(enqueue_time, 8))) return RLVLA_ERR_INVALID_ARG;
   if (obs_src && misaligned(obs_src, 16)) return RLVLA_ERR_INVALID_ARG;
+  if (q->obs_fifo && q->obs_bytes > 0 && n > 0 && !obs_src) return RLVLA_ERR_INVALID_ARG;
   if (n == 0) return RLVLA_OK;
   if (!device_ready()) return RLVLA_ERR_CUDA;
   BatchOfferArgs a{*q, env_id, enqueue_time, n, now, static_cast<const uint8_t*>(obs_src),
@@ -398,6 +401,7 @@ RLVLA_API rlvla_status rlvla_batch_poll(const rlvla_batch_queue* q, int64_t now,
   if ((st = check_ws(workspace, ws_bytes)) != RLVLA_OK) return st;
   if (b_max < 1 || t_max < 0 || now < 0 || !out_env || !out_time || !out_n)
     return RLVLA_ERR_INVALID_ARG;
+  if (q->obs_fifo && b_max > q->max_batch) return RLVLA_ERR_INVALID_ARG;
   if (misaligned(out_time, 8) || misaligned(out_env, 4) || misaligned(out_n, 4) ||
       (out_obs && misaligned(out_obs, 16)))
     return RLVLA_ERR_INVALID_ARG;

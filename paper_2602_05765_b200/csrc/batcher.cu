@@ -138,9 +138,18 @@ __global__ void __launch_bounds__(kMaxOffer) batch_offer_kernel(BatchOfferArgs a
     const int64_t ob16 = ob >> 4;
     uint4* slots = reinterpret_cast<uint4*>(a.q.obs);
     const uint4* src = reinterpret_cast<const uint4*>(a.obs_src);
-    grid_copy_rows(
-        nacc, ob16, [&](int k) { return slots + int64_t(s_cand[s_idx[k]]) * ob16; },
-        [&](int k) { return src + int64_t(s_idx[k]) * ob16; });
+    if (a.q.obs_fifo) {
+      // FIFO rows: request k of this call lands at ring position tail + k
+      const int64_t tail = s_state[1];
+      const int cap = a.q.n_env;
+      grid_copy_rows(
+          nacc, ob16, [&](int k) { return slots + ((tail + k) % cap) * ob16; },
+          [&](int k) { return src + int64_t(s_idx[k]) * ob16; });
+    } else {
+      grid_copy_rows(
+          nacc, ob16, [&](int k) { return slots + int64_t(s_cand[s_idx[k]]) * ob16; },
+          [&](int k) { return src + int64_t(s_idx[k]) * ob16; });
+    }
   }
   const int n_oob = __syncthreads_count(code == 0);
   const int n_fut = __syncthreads_count(code == 1);
@@ -185,12 +194,22 @@ __global__ void __launch_bounds__(kPollThreads) batch_poll_kernel(BatchPollArgs 
     for (int k = threadIdx.x; k < b; k += blockDim.x) s_env[k] = a.q.ring_env[(head + k) % cap];
     __syncthreads();
   }
+  const int64_t row0 = head % cap;  // FIFO rows: the batch starts here
+  if (a.q.obs_fifo && ob > 0 && row0 + b > cap) {
+    // the batch wraps: mirror its first rows past n_env so rows [row0, row0 + b) are contiguous
+    const int64_t ob16 = ob >> 4;
+    uint4* rows = reinterpret_cast<uint4*>(a.q.obs);
+    grid_copy_rows(
+        int(row0 + b - cap), ob16, [&](int k) { return rows + (int64_t(cap) + k) * ob16; },
+        [&](int k) { return rows + int64_t(k) * ob16; });
+  }
   if (a.out_obs != nullptr && ob > 0) {
     const int64_t ob16 = ob >> 4;
     const uint4* slots = reinterpret_cast<const uint4*>(a.q.obs);
     uint4* out = reinterpret_cast<uint4*>(a.out_obs);
     auto dst = [&](int k) { return out + int64_t(k) * ob16; };
     auto src = [&](int k) {
+      if (a.q.obs_fifo) return slots + ((head + k) % cap) * ob16;
       const int env = staged ? s_env[k] : a.q.ring_env[(head + k) % cap];
       return slots + int64_t(env) * ob16;
     };
@@ -211,6 +230,7 @@ __global__ void __launch_bounds__(kPollThreads) batch_poll_kernel(BatchPollArgs 
       a.q.state[0] = head + b;
       if (p - b > 0) a.q.state[2] = a.now;  // requests remain: re-anchor at the poll time
       a.q.state[3] = nbatches + 1;
+      a.q.state[4] = row0;
     }
     *a.out_n = b;
     a.ws.ctrl[CTRL_BPOLL] = 0u;
@@ -251,7 +271,8 @@ cudaError_t launch_batch_offer(const BatchOfferArgs& a, cudaStream_t s) {
 
 cudaError_t launch_batch_poll(const BatchPollArgs& a, cudaStream_t s) {
   const int64_t rows = a.b_max < a.q.n_env ? a.b_max : a.q.n_env;
-  const int grid = (a.out_obs != nullptr && a.q.obs_bytes > 0) ? copy_grid(rows, a.q.obs_bytes, kPollCtasPerSm) : 1;
+  const bool copies = a.q.obs_bytes > 0 && (a.out_obs != nullptr || a.q.obs_fifo);
+  const int grid = copies ? copy_grid(rows, a.q.obs_bytes, kPollCtasPerSm) : 1;
   return launch_pdl(batch_poll_kernel, grid, kPollThreads, a, s);
 }
 

@@ -102,6 +102,34 @@ def main():
     torch.cuda.synchronize()
     tick_us = e0.elapsed_time(e1) * 1e3 / (a.iters - 3)
     assert int(out_n.item()) == B
+    # staged arrivals (CPU simulators: observations come through a device staging buffer, so
+    # every offer carries obs_src): per tick, offer 64 with payload + one firing poll, for the
+    # env-slot queue (copy into slots, gather at poll) and the FIFO-row queue (copy into FIFO
+    # rows at offer, the batch read in place)
+    staged = {}
+    stg = torch.randint(0, 256, (B, ob), dtype=torch.uint8, device="cuda")
+    for fifo in (False, True):
+        q3 = P.BatchQueue.allocate(E2, ob, obs_fifo=fifo, max_batch=B if fifo else 0)
+        oo = None if fifo else out_obs
+        for i in range(3):
+            P.rlvla_batch_offer(q3, perms2[i % 16], t2[i], i, cnt, obs_src=stg, ws=ws)
+            P.rlvla_batch_poll(q3, i, B, 10, out_env, out_time, out_n, out_obs=oo, ws=ws)
+        torch.cuda.synchronize()
+        torch.cuda._sleep(200_000_000)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for i in range(3, a.iters):
+            P.rlvla_batch_offer(q3, perms2[i % 16], t2[i], i, cnt, obs_src=stg, ws=ws)
+            P.rlvla_batch_poll(q3, i, B, 10, out_env, out_time, out_n, out_obs=oo, ws=ws)
+        e1.record(s)
+        torch.cuda.synchronize()
+        staged["fifo_rows" if fifo else "env_slots"] = {
+            "us_per_tick": e0.elapsed_time(e1) * 1e3 / (a.iters - 3),
+            "bytes_per_tick": (2 if fifo else 4) * B * ob}
+        del q3
+    for v in staged.values():
+        v["GBps"] = v["bytes_per_tick"] / v["us_per_tick"] / 1e3
+    assert int(out_n.item()) == B
     byts = 2 * B * ob
     pm = sorted(poll_ms)[len(poll_ms) // 2]
     print(json.dumps({"what": "rlvla_batch_poll (Eq. (1) trigger + gather)", "n_env": E, "b_max": B,
@@ -111,6 +139,7 @@ def main():
                       "idle_poll_us_median": sorted(idle)[len(idle) // 2] * 1e3,
                       "torch_index_select_us_median": sorted(ref)[len(ref) // 2] * 1e3,
                       "tick_loop": {"n_env": E2, "us_per_tick": tick_us, "GBps": byts / tick_us / 1e3},
+                      "staged_tick_loop": staged,
                       "l2": "flushed (256 MB read) before every single-call iteration; the tick "
                             "loop's slots (> 512 MB) exceed L2"}))
 
