@@ -411,10 +411,10 @@ RLVLA_API rlvla_status rlvla_comm_destroy(rlvla_comm c);
  * memory (every rank's mailbox mapped through CUDA IPC at rlvla_comm_init; the kernel's last
  * CTA pushes its slots to all ranks and sums them in rank order): C1 and the GRPO returns
  * allgather C2 in rlvla_advantages (n_env_global <= 32768), C3 in rlvla_logprob_fwd_bwd,
- * token-level rlvla_ppo_loss and rlvla_flow_logprob. 0 when those calls use NCCL
+ * rlvla_ppo_loss and rlvla_flow_logprob. 0 when those calls use NCCL
  * collectives after the kernel. RLVLA_P2P=0 at init forces NCCL. Calls with one communicator
  * must be stream-ordered and made in the same order on every rank (as for NCCL). The
- * value loss reduces slots 19..21 the same way; the chunk-ratio path always uses NCCL. */
+ * value loss reduces slots 19..21 and the chunk-ratio path slots 6..17 the same way. */
 RLVLA_API int32_t rlvla_comm_p2p_enabled(rlvla_comm c);
 
 RLVLA_API const char* rlvla_status_string(rlvla_status s);

@@ -302,8 +302,8 @@ RLVLA_API rlvla_status rlvla_ppo_loss(const float* logp, int64_t rows, const int
   a.loss_tok = loss_tok;
   a.stats = stats;
   if (workspace) a.ws = carve(workspace);
-  // token-level path: in-kernel NVLink reduction; the chunk-level path keeps NCCL
-  const bool p2p = stats && f->ratio_level == 0 && uses_p2p(comm);
+  // C3 in-kernel over NVLink (token- and chunk-level paths)
+  const bool p2p = stats && uses_p2p(comm);
   if (p2p) a.ws.p2p = p2p_desc(comm, P2P_CH_LOSS);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   st = cuda_status(launch_ppo_loss(a, s));

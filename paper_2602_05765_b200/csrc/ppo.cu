@@ -150,13 +150,17 @@ __global__ void __launch_bounds__(256) ppo_chunk_kernel(PpoArgs a, PpoConst pc) 
   if (last_block_reduce(a.ws.ctrl + CTRL_PPO, a.ws.partials, kLossSlots, tot)) {
     const double Ns = a.f.tok_denominator > 0.0 ? a.f.tok_denominator : tot[9];
     const double inv = Ns > 0.0 ? 1.0 / Ns : 0.0;
+    __syncthreads();
     if (threadIdx.x < kLossSlots && a.stats) {
       double v = tot[threadIdx.x];
       if (threadIdx.x == 0 || threadIdx.x == 11) v *= inv;
       if (threadIdx.x == 9) v = 0.0;  // KL_REF_SUM: no reference term on this path
       if (a.f.accumulate) v += a.stats[RLVLA_STAT_LOSS + threadIdx.x];
-      a.stats[RLVLA_STAT_LOSS + threadIdx.x] = v;
+      tot[threadIdx.x] = v;
     }
+    __syncthreads();
+    if (a.stats && a.ws.p2p.nranks > 1) p2p_exchange(tot, kLossSlots, a.ws.p2p);  // C3 in-kernel
+    if (threadIdx.x < kLossSlots && a.stats) a.stats[RLVLA_STAT_LOSS + threadIdx.x] = tot[threadIdx.x];
     if (threadIdx.x == 0) {
       if (a.stats) a.stats[RLVLA_STAT_DENOM] = Ns;
       *chunk_scratch(a) = inv;

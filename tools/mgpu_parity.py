@@ -166,6 +166,24 @@ def main():
     s5 = st5.cpu().numpy()
     assert abs(s5[6] - rf[0].item()) <= 1e-4 * max(1e-3, abs(rf[0].item())), (s5[6], rf[0].item())
     assert s5[11] == rf[1].item() and s5[18] == Nf
+    # NEXT-2 chunk-level ratio through rlvla_ppo_loss (explicit denominator), C3 over the ranks
+    S, A2 = 200, 56
+    Rc = S * A2
+    lpc = rng.normal(-4, 1, Rc).astype(np.float32)
+    lbc = (lpc - rng.normal(0, 0.004, Rc)).astype(np.float32)
+    advc = rng.normal(size=S).astype(np.float32)
+    gc = torch.empty(Rc, device=dev)
+    st6 = torch.zeros(24, dtype=torch.float64, device=dev)
+    fa = P.ppo_args(logp_behav=cu(lbc), adv=cu(advc), version=cu(np.full(S, CUR, np.int32)),
+                    slot_key=cu(np.ones(S, np.int64)), a_tok=A2, cur_version=CUR, ratio_level=1,
+                    tok_denominator=1000.0)
+    P.rlvla_ppo_loss(cu(lpc), None, fa, gc, None, st6, ws, comm=comm)
+    oc = O_ppo.ppo_loss_chunk(lpc, lbc, advc, np.ones(Rc, bool), np.arange(Rc) // A2, S, n_den=1000.0)
+    H.assert_close_rel(gc.cpu().numpy(), oc["grad"], 1e-4, 1e-9, "chunk grad")
+    rc = torch.tensor([oc["stats"]["loss"]], dtype=torch.float64, device=dev)
+    dist.all_reduce(rc)
+    s6 = st6.cpu().numpy()
+    assert abs(s6[6] - rc[0].item()) <= 1e-4 * max(1e-3, abs(rc[0].item())), (s6[6], rc[0].item())
     dist.barrier()
     if rank == 0:
         print(f"MGPU PARITY OK world={world} nccl={P.rlvla_nccl_version()} "
