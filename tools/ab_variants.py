@@ -15,7 +15,7 @@ VARIANTS = {
 }
 # name -> git revision whose csrc/ + include/ are built as one more variant
 # (the ABI only grew at the end of its structs, so today's binding drives older libraries)
-REVISIONS = {"prev": "HEAD"}  # e.g. {"pre_next2": "6cd809f"}
+REVISIONS = {}  # e.g. {"prev": "HEAD"} builds the last commit as a variant
 
 
 def build_revision(name, rev):
