@@ -10,10 +10,12 @@
 //                       (range, enqueue_time <= now, not pending, first of its env in the
 //                       call) and the FIFO positions (ballot prefix sum); with obs_src the
 //                       grid (one CTA per SM) copies the accepted observations into their
-//                       env slots; the last CTA appends to the ring.
+//                       env slots (obs_fifo = 0) or their FIFO rows (obs_fifo = 1); the
+//                       last CTA appends to the ring.
 //   batch_poll_kernel   every CTA evaluates Eq. (1) from the same state; a poll that does
 //                       not fire returns at once. Otherwise the b = min(p, B_max) oldest
-//                       observations are gathered into the batch, the concatenated rows
+//                       observations are gathered into the batch (FIFO rows: already in
+//                       place, only a wrap is mirrored past n_env), the concatenated rows
 //                       split evenly over one CTA per SM (128-bit loads/stores: one read
 //                       + one write of b * obs_bytes, HBM-bound); the last CTA pops the
 //                       ring. (Measured and rejected: TMA bulk copies through an SMEM ring,

@@ -2,16 +2,19 @@
 // K Gaussian denoising transitions (reading R25; pi_0 / pi_0.5 / GR00T, P:39, P:77, P:99,
 // Table 2 "Model Num Step" = 4), optionally fused with the PPO epilogue and its backward.
 //
-// One warp per decision step (row): the row's n = K*D elements are read once with 4-wide
-// vector loads (mu in f32 or bf16, x, optional ln sigma), z = (x - mu)/sigma and 1/sigma are
-// kept in registers (16 elements per lane, rows up to 512 elements with n % 4 == 0; other
-// rows take a scalar loop that re-reads in the backward pass); a sigma schedule becomes a
-// per-element 1/sigma table in SMEM, so there is no division in the loops, and
-//   logp = -0.5 sum z^2 - sum ln sigma - n ln(2 pi)/2,   H = sum ln sigma + n (ln 2 pi + 1)/2
-// are warp sums (fp32 lane partials, fp64 across lanes; with a sigma schedule the ln sigma
-// sum is D sum_k ln sigma_k, computed once per CTA in fp64). Every lane then evaluates the
-// shared PPO epilogue (epilogue.cuh) on the warp-uniform sums, and the backward writes
-//   dmu = g z / sigma,   dln sigma = g (z^2 - 1) - c     (c = ent_coef m / N)
+// Warp tiles of kTile = 4 decision steps (flow_kernel; the launch picks a compile-time row
+// length for the paper's K x D shapes, 280 and 140):
+//   pass 1  step by step, the row's n = K*D elements are streamed with 4-wide loads (mu in
+//           f32 or bf16, x, optional ln sigma; a sigma schedule is a per-element 1/sigma
+//           table in SMEM, so there is no division) and packed fp32x2 math; each lane's
+//           partial sum of z^2 (and ln sigma) goes to SMEM [step][lane]
+//   epilogue lane t owns step t of the tile: it sums the 32 partials in fixed order in fp64,
+//           forms logp = -0.5 sum z^2 - sum ln sigma - n ln(2 pi)/2 and
+//           H = sum ln sigma + n (ln 2 pi + 1)/2, and runs the shared PPO epilogue
+//           (epilogue.cuh) — the per-step scalar work spread over the lanes
+//   pass 2  step by step, g and c are broadcast and the backward re-reads the row (L1/L2):
+//           dmu = g z / sigma,   dln sigma = g (z^2 - 1) - c     (c = ent_coef m / N)
+// Rows whose length is not a multiple of 4 (or unaligned pointers) take scalar loops.
 // Bytes per row: n (|mu| + 4 [+ 4 ln sigma]) read, n |mu| [+ 4 n] written.
 #include "epilogue.cuh"
 
