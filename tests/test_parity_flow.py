@@ -153,3 +153,28 @@ def test_external_backward():
     fin = np.isfinite(gr["dmu"]).all(axis=(1, 2))
     H.assert_close_rel(dmu.cpu().numpy()[fin], gr["dmu"][fin], 1e-5, 1e-30, "dmu")
     H.assert_close_rel(dls.cpu().numpy()[fin], gr["dlog_std"][fin], 1e-5, np.abs(g[fin])[:, None, None], "dlog_std")
+
+
+def test_rerun_bit_identical():
+    """Fixed-order reductions: two identical fused calls give identical bits."""
+    P = _P()
+    R, K, D = 500, 4, 70
+    mu, mu64, x, ls = _case(R, K, D, torch.bfloat16, False, seed=9)
+    rng = np.random.default_rng(3)
+    lb = (np.nan_to_num(F.chain_logprob(mu64, x, sigma_k=SIG_K)["logp"]) - rng.normal(0, 0.05, R)).astype(np.float32)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    outs = []
+    for _ in range(2):
+        g = torch.empty(R, device="cuda")
+        fa = P.ppo_args(logp_behav=cu(lb), adv=cu(rng.normal(size=R).astype(np.float32) * 0 + 0.7),
+                        version=cu(np.full(R, 100, np.int32)), slot_key=cu(np.ones(R, np.int64)),
+                        a_tok=1, cur_version=100, tok_denominator=float(R), out_grad_logp=g)
+        ch = P.GaussChain(mu.cuda(), cu(x), cu(SIG_K))
+        logp = torch.empty(R, device="cuda")
+        dmu = torch.empty_like(ch.mu)
+        st = torch.zeros(24, dtype=torch.float64, device="cuda")
+        P.rlvla_flow_logprob(ch, logp=logp, fused=fa, dmu=dmu, stats=st, ws=P.workspace(1))
+        outs.append((logp.view(torch.int32).cpu(), g.view(torch.int32).cpu(), dmu.view(torch.int16).cpu(),
+                     st.view(torch.int64).cpu()))
+    for a_, b_ in zip(*outs):
+        assert torch.equal(a_, b_)  # bitwise (the crafted non-finite step included)
