@@ -27,9 +27,9 @@ namespace rlvla {
 
 const DeviceInfo& device_info() {
   static std::mutex mu;
-  static DeviceInfo cache[64];
+  static DeviceInfo cache[kMaxDevices];
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
     static DeviceInfo none;
     return none;
   }

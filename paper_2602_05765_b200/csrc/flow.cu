@@ -356,12 +356,15 @@ template <typename T, int MODE, bool VEC, int NQ>
 cudaError_t launch_m(const FlowArgs& a, cudaStream_t s) {
   const int n = a.c.n_steps * a.c.dim;
   const size_t smem = flow_smem(n);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && attr < smem) {
+  static size_t attr[kMaxDevices] = {};  // the SMEM opt-in is a per-device attribute
+  const int dev = device_info().device;
+  size_t dummy = 0;
+  size_t& cached = (dev >= 0 && dev < kMaxDevices) ? attr[dev] : dummy;
+  if (smem > 48 * 1024 && cached < smem) {
     cudaError_t e = cudaFuncSetAttribute(flow_kernel<T, MODE, VEC, NQ>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    attr = smem;
+    cached = smem;
   }
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel<T, MODE, VEC, NQ>,

@@ -314,6 +314,7 @@ __device__ __forceinline__ void p2p_allreduce(double* vals, int n, const P2PDesc
 // ------------------------------------------------------------------------------------
 // host side
 // ------------------------------------------------------------------------------------
+constexpr int kMaxDevices = 64;  // per-device host caches
 struct DeviceInfo {
   int device = -1;
   int sm_count = 0;

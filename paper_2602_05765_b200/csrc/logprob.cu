@@ -876,15 +876,19 @@ cudaError_t launch_mode(const LpArgs& a, Lp p, cudaStream_t s) {
                               : reinterpret_cast<const void*>(lp_tma_kernel<MODE, true, 0>))
                         : (f7 ? reinterpret_cast<const void*>(lp_tma_kernel<MODE, false, 7>)
                               : reinterpret_cast<const void*>(lp_tma_kernel<MODE, false, 0>));
-    static int attr_dyn[3][2][2] = {};
-    if (attr_dyn[MODE][xp][f7] < int(smem)) {
+    // the opt-in SMEM limit is a per-device function attribute: cached per device
+    static int attr_dyn[kMaxDevices][3][2][2] = {};
+    const int dev = device_info().device;
+    int dummy = 0;
+    int& cached = (dev >= 0 && dev < kMaxDevices) ? attr_dyn[dev][MODE][xp][f7] : dummy;
+    if (cached < int(smem)) {
       cudaFuncAttributes fa{};
       cudaError_t e = cudaFuncGetAttributes(&fa, fn);
       if (e != cudaSuccess) return e;
       if (smem + fa.sharedSizeBytes > size_t(device_info().smem_optin)) return cudaErrorInvalidConfiguration;
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
-      attr_dyn[MODE][xp][f7] = int(smem);
+      cached = int(smem);
     }
     int grid = int(R < sms ? R : sms);
     if (xp) {
