@@ -558,7 +558,10 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
                 const uint32_t c = bmax2_nan(w4[q], kNegClampPair);
                 const float2 t2 = __ffma2_rn(make_float2(bf_lo(c), bf_hi(c)), make_float2(L2E, L2E),
                                              make_float2(nML, nML));
-                const float2 f2 = __ffma2_rn(make_float2(rsv.k2, rsv.k2), t2, make_float2(rsv.k1, rsv.k1));
+                // external bwd: k2 = 0, dx = k1 2^t (no entropy term to add)
+                const float2 f2 = MODE == MODE_BWD ? make_float2(rsv.k1, rsv.k1)
+                                                   : __ffma2_rn(make_float2(rsv.k2, rsv.k2), t2,
+                                                                make_float2(rsv.k1, rsv.k1));
                 const float2 d2 = __fmul2_rn(make_float2(ex2(t2.x), ex2(t2.y)), f2);
                 ow[q] = pack_bf16x2(d2.x, d2.y);
               }
