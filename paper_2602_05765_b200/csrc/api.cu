@@ -10,7 +10,18 @@
 #include <vector>
 #include <mutex>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.cuh"
+
+namespace {
+// NVTX range around each entry point (header-only NVTX3: free when no tool is attached), so
+// an nsys timeline groups the kernels and collectives of a call under its ABI name
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 struct rlvla_comm_s {
   ncclComm_t comm;
@@ -163,6 +174,7 @@ RLVLA_API size_t rlvla_workspace_bytes(int64_t rows, int32_t n_env_global, int32
 RLVLA_API rlvla_status rlvla_scatter_steps(const rlvla_traj_buffer* buf,
                                            const rlvla_step_batch* rec, int32_t cur_version,
                                            uint64_t seq_base, int64_t* counters, void* stream) {
+  NvtxRange nvtx_range("rlvla_scatter_steps");
   rlvla_status st = check_buffer(buf);
   if (st != RLVLA_OK) return st;
   if (!rec || rec->n_rec < 0 || !counters) return RLVLA_ERR_INVALID_ARG;
@@ -189,6 +201,7 @@ RLVLA_API rlvla_status rlvla_advantages(const rlvla_traj_buffer* buf, const floa
                                         const rlvla_adv_params* p, float* adv, float* ret,
                                         double* stats, void* workspace, size_t ws_bytes,
                                         rlvla_comm comm, void* stream) {
+  NvtxRange nvtx_range("rlvla_advantages");
   rlvla_status st = check_buffer(buf);
   if (st != RLVLA_OK) return st;
   if (!p || !adv || !stats || !workspace) return RLVLA_ERR_INVALID_ARG;
@@ -234,6 +247,7 @@ RLVLA_API rlvla_status rlvla_logprob_fwd_bwd(const rlvla_logits* x, const int32_
                                              const rlvla_ppo_args* fused, void* dlogits,
                                              double* stats, void* workspace, size_t ws_bytes,
                                              rlvla_comm comm, void* stream) {
+  NvtxRange nvtx_range("rlvla_logprob_fwd_bwd");
   if (!x || !x->ptr || !target) return RLVLA_ERR_INVALID_ARG;
   if (x->dtype != RLVLA_F32 && x->dtype != RLVLA_BF16) return RLVLA_ERR_INVALID_ARG;
   if (x->rows < 0 || x->vocab < 1 || x->ld < x->vocab) return RLVLA_ERR_INVALID_ARG;
@@ -283,6 +297,7 @@ RLVLA_API rlvla_status rlvla_ppo_loss(const float* logp, int64_t rows, const int
                                       const rlvla_ppo_args* f, float* grad_logp, float* loss_tok,
                                       double* stats, void* workspace, size_t ws_bytes,
                                       rlvla_comm comm, void* stream) {
+  NvtxRange nvtx_range("rlvla_ppo_loss");
   if (!logp || !f || !grad_logp || rows < 0) return RLVLA_ERR_INVALID_ARG;
   rlvla_status st = check_ppo_args(f);
   if (st != RLVLA_OK) return st;
@@ -323,6 +338,7 @@ RLVLA_API rlvla_status rlvla_value_loss(const float* v_new, const float* v_old, 
                                         double denominator, float* grad_v, float* loss_step,
                                         double* stats, void* workspace, size_t ws_bytes,
                                         rlvla_comm comm, void* stream) {
+  NvtxRange nvtx_range("rlvla_value_loss");
   if (!v_new || !ret || !slot_key || !version || !grad_v || n_steps < 0 || max_staleness < 0)
     return RLVLA_ERR_INVALID_ARG;
   if (clip_eps > 0.f && !v_old) return RLVLA_ERR_INVALID_ARG;
@@ -370,6 +386,7 @@ RLVLA_API rlvla_status rlvla_batch_offer(const rlvla_batch_queue* q, const int32
                                          const int64_t* enqueue_time, int32_t n, int64_t now,
                                          const void* obs_src, int64_t* counters,
                                          void* workspace, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_range("rlvla_batch_offer");
   rlvla_status st = check_queue(q);
   if (st != RLVLA_OK) return st;
   if ((st = check_ws(workspace, ws_bytes)) != RLVLA_OK) return st;
@@ -396,6 +413,7 @@ RLVLA_API rlvla_status rlvla_batch_poll(const rlvla_batch_queue* q, int64_t now,
                                         int64_t t_max, int32_t* out_env, int64_t* out_time,
                                         void* out_obs, int32_t* out_n, void* workspace,
                                         size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_range("rlvla_batch_poll");
   rlvla_status st = check_queue(q);
   if (st != RLVLA_OK) return st;
   if ((st = check_ws(workspace, ws_bytes)) != RLVLA_OK) return st;
@@ -416,6 +434,7 @@ RLVLA_API rlvla_status rlvla_flow_logprob(const rlvla_gauss_chain* c, float* log
                                           void* dmu, float* dlog_std, double* stats,
                                           void* workspace, size_t ws_bytes, rlvla_comm comm,
                                           void* stream) {
+  NvtxRange nvtx_range("rlvla_flow_logprob");
   if (!c || c->rows < 0 || c->n_steps < 1 || c->dim < 1 || !c->mu || !c->x)
     return RLVLA_ERR_INVALID_ARG;
   if (int64_t(c->n_steps) * c->dim > kFlowMaxElems) return RLVLA_ERR_INVALID_ARG;

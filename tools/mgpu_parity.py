@@ -3,7 +3,9 @@ each rank scatters the records it owns, computes GRPO (groups spanning ranks: C2
 allgather + C1 allreduce) and GAE+global whitening advantages, and the fused loss with the
 C3 allreduce, all through the C ABI with the library's NCCL communicator; the result is
 compared with the oracle on the same shard using the same sharding helpers. Then the value
-loss (slots 19..21) and the flow-policy chain loss (C3) with a global denominator.
+loss (slots 19..21) and the flow-policy chain loss (C3) with a global denominator, and rank
+invariance: the same global problem on one rank vs sharded gives bit-identical GRPO advantages
+and per-row logp / grad / dlogits, and loss statistics within 1e-12.
 
   torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/mgpu_parity.py
 """
@@ -121,6 +123,43 @@ def main():
     assert abs(s3[6] - rs[0]) <= 1e-5 * max(1e-3, abs(rs[0])), (s3[6], rs[0])
     assert s3[11] == rs[1] and abs(s3[9] - rs[2]) <= 1e-5 * abs(rs[2])
     assert s3[18] == tot[1].item()
+    # ---- rank invariance: the same global problem on ONE rank vs sharded ----
+    # GRPO advantages and every per-row output bit-identical; global stats within 1e-12
+    full_batch = P.StepBatch(*(t(a_) for a_ in (rec.env_id, rec.step, rec.version, rec.reward, rec.done,
+                                                rec.value, rec.tokens, lb)))
+    buf_f = P.TrajectoryBuffer.allocate(E, T, A, device=dev)
+    P.rlvla_scatter_steps(buf_f, full_batch, CUR, 1, torch.zeros(4, dtype=torch.int64, device=dev))
+    adv_f = torch.zeros(E, T, device=dev)
+    st_f = torch.zeros(24, dtype=torch.float64, device=dev)
+    ws_f = P.workspace(E, device=dev)
+    P.rlvla_advantages(buf_f, t(traj.last_value), P.adv_params("grpo", group_id=gid, group_size=4,
+                       n_env_global=E, cur_version=CUR), adv_f, torch.zeros(E, T, device=dev), st_f, ws_f)
+    adv_d = torch.zeros(E_r, T, device=dev)
+    st_d = torch.zeros(24, dtype=torch.float64, device=dev)
+    P.rlvla_advantages(buf, lv, P.adv_params("grpo", group_id=gid, group_size=4, env_offset=lo,
+                                             n_env_global=E, cur_version=CUR), adv_d, ret, st_d, ws,
+                       comm=comm)
+    assert torch.equal(adv_d.view(torch.int32), adv_f[lo:hi].view(torch.int32)), "GRPO adv not rank-invariant"
+    assert torch.equal(st_d[:6], st_f[:6])
+    xf = torch.from_numpy(x.astype(np.float32)).to(dev)
+    outs = {}
+    for name, (bb, aa, xx, ss, cm) in {"full": (buf_f, adv_f, xf, st_f, None),
+                                       "shard": (buf, adv_d, xr, st_d, comm)}.items():
+        n_ = xx.shape[0]
+        lp_, g_ = torch.empty(n_, device=dev), torch.empty(n_, device=dev)
+        dx_ = torch.empty_like(xx)
+        so = torch.zeros(24, dtype=torch.float64, device=dev)
+        fa_ = P.ppo_args(logp_behav=bb.logp_behav.view(-1), adv=aa.view(-1), version=bb.version.view(-1),
+                         slot_key=bb.slot_key.view(-1), a_tok=A, cur_version=CUR, adv_stats=ss, out_grad_logp=g_)
+        P.rlvla_logprob_fwd_bwd(xx, bb.tokens.view(-1), logp=lp_, fused=fa_, dlogits=dx_, stats=so,
+                                ws=ws_f if cm is None else ws, comm=cm)
+        outs[name] = (lp_, g_, dx_, so)
+    r0, r1 = lo * T * A, hi * T * A
+    for k_ in range(3):
+        assert torch.equal(outs["full"][k_][r0:r1].view(torch.int32), outs["shard"][k_].view(torch.int32)), k_
+    sf, sd = outs["full"][3].cpu().numpy(), outs["shard"][3].cpu().numpy()
+    for k_ in range(6, 18):
+        assert abs(sf[k_] - sd[k_]) <= 1e-12 * max(1.0, abs(sf[k_])), (k_, sf[k_], sd[k_])
     # NEXT-2 value loss: per-rank steps, explicit global N_v, slots 19..21 allreduced
     from oracle import flow as O_fl
     from oracle import ppo as O_ppo
