@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--eager", action="store_true",
                     help="launch the timed steps eagerly instead of one captured CUDA graph")
     ap.add_argument("--ref-envs", type=int, default=1, help="envs per reference-arm step")
+    ap.add_argument("--trace", default=None,
+                    help="write a chrome-trace JSON of the timed steps' stage events (rank 0)")
     return ap.parse_args()
 
 
@@ -318,6 +320,22 @@ def run_ours(args):
     k_ms = [cr.elapsed(a, b) for a, b in zip(ev_k0, ev_k1)]   # one per fused launch
     sc_ms = sorted(cr.elapsed(a, b) for a, b in zip(ev_sa, ev_sb))
     ad_ms = sorted(cr.elapsed(a, b) for a, b in zip(ev_sb, ev_sc))
+    if args.trace and rank == 0:
+        # chrome://tracing / Perfetto: one complete event per stage of every timed step,
+        # timestamps relative to the start of the timed region (CUDA events, microseconds)
+        evs = []
+        for i in range(args.steps):
+            t_s = cr.elapsed(ev_t0, ev_sa[i]) * 1e3
+            evs.append(dict(name="S1 scatter (64 chunks)", ph="X", pid=0, tid=0, ts=t_s,
+                            dur=cr.elapsed(ev_sa[i], ev_sb[i]) * 1e3))
+            evs.append(dict(name="S2 advantages", ph="X", pid=0, tid=0, ts=cr.elapsed(ev_t0, ev_sb[i]) * 1e3,
+                            dur=cr.elapsed(ev_sb[i], ev_sc[i]) * 1e3))
+            for j in range(nmb):
+                a_, b_ = ev_k0[i * nmb + j], ev_k1[i * nmb + j]
+                evs.append(dict(name=f"S3+S4 fused (micro-batch {j})", ph="X", pid=0, tid=0,
+                                ts=cr.elapsed(ev_t0, a_) * 1e3, dur=cr.elapsed(a_, b_) * 1e3))
+        with open(args.trace, "w") as f:
+            json.dump({"traceEvents": evs, "displayTimeUnit": "ms"}, f)
     st_host = lstats.cpu().numpy()
     cnt = counters.cpu().numpy()
 
