@@ -2,19 +2,21 @@
 // K Gaussian denoising transitions (reading R25; pi_0 / pi_0.5 / GR00T, P:39, P:77, P:99,
 // Table 2 "Model Num Step" = 4), optionally fused with the PPO epilogue and its backward.
 //
-// Warp tiles of kTile = 4 decision steps (flow_kernel; the launch picks a compile-time row
-// length for the paper's K x D shapes, 280 and 140):
-//   pass 1  step by step, the row's n = K*D elements are streamed with 4-wide loads (mu in
-//           f32 or bf16, x, optional ln sigma; a sigma schedule is a per-element 1/sigma
-//           table in SMEM, so there is no division) and packed fp32x2 math; each lane's
-//           partial sum of z^2 (and ln sigma) goes to SMEM [step][lane]
-//   epilogue lane t owns step t of the tile: it sums the 32 partials in fixed order in fp64,
-//           forms logp = -0.5 sum z^2 - sum ln sigma - n ln(2 pi)/2 and
+// Warp tiles of kTile = 4 decision steps:
+//   pass 1  step by step, the row's n = K*D elements are read with 4-wide loads (mu in f32 or
+//           bf16, x, optional ln sigma; a sigma schedule is a per-element 1/sigma table in
+//           SMEM, so there is no division) and packed fp32x2 math; each lane keeps its partial
+//           sums of z^2 (and ln sigma) of the four steps in registers
+//   epilogue a fixed fp64 butterfly (row_totals4) leaves step t's totals at lane t, which forms
+//           logp = -0.5 sum z^2 - sum ln sigma - n ln(2 pi)/2 and
 //           H = sum ln sigma + n (ln 2 pi + 1)/2, and runs the shared PPO epilogue
 //           (epilogue.cuh) — the per-step scalar work spread over the lanes
-//   pass 2  step by step, g and c are broadcast and the backward re-reads the row (L1/L2):
-//           dmu = g z / sigma,   dln sigma = g (z^2 - 1) - c     (c = ent_coef m / N)
-// Rows whose length is not a multiple of 4 (or unaligned pointers) take scalar loops.
+//   pass 2  step by step, g and c are broadcast and the backward writes
+//           dmu = g (z / sigma),   dln sigma = g (z^2 - 1) - c     (c = ent_coef m / N)
+// Two kernels run this tile: flow_tma_kernel for the paper's K x D shapes (280, 140 elements;
+// each warp's tiles staged HBM -> SMEM by bulk copies kFlowStages tiles ahead, pass 1 leaving
+// z / sigma in place for pass 2) and flow_kernel for any other shape (direct loads; rows whose
+// length is not a multiple of 4, or unaligned pointers, take scalar loops).
 // Bytes per row: n (|mu| + 4 [+ 4 ln sigma]) read, n |mu| [+ 4 n] written.
 #include "epilogue.cuh"
 
@@ -68,20 +70,35 @@ __device__ __forceinline__ void st_mu4<__nv_bfloat16>(void* p, int64_t i, float4
       make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
 }
 
-#ifndef RLVLA_FLOW_TILE
-#define RLVLA_FLOW_TILE 4  // rows per warp tile (<= 32): one lane runs each row's epilogue
-#endif
-constexpr int kTile = RLVLA_FLOW_TILE;
-constexpr int kPad = 33;  // partials [row][lane] padded: conflict-free row-wise reads
 
+constexpr int kTile = 4;  // decision steps per warp tile: lane t < 4 runs step t's epilogue
+
+// a row's PPO inputs as loaded: kept raw (the key is not compared yet) so that no
+// instruction consumes a load before pass 1 has run — the loads' latency hides behind it
 struct RowMeta4 {
   float lpb = 0.f, lpp = 0.f, lref = 0.f, adv = 0.f;
   int ver = 0;
-  bool valid = true;
+  unsigned long long key = 1ull;
 };
 
+// The four rows' totals of the lanes' fp32 partials, in fp64: a butterfly reduce-scatter
+// (xor 16 halves the rows each lane carries, xor 8 halves them again, xor 4/2/1 finish row
+// (lane >> 3) & 3), then lane t < 4 fetches row t. A fixed tree: the bits do not depend on
+// timing or on which warp runs the tile.
+__device__ __forceinline__ double row_totals4(const float (&v)[kTile], int lane) {
+  const bool h = lane & 16, b = lane & 8;
+  const double d0 = v[0], d1 = v[1], d2 = v[2], d3 = v[3];
+  const double e0 = (h ? d2 : d0) + __shfl_xor_sync(0xffffffffu, h ? d0 : d2, 16);
+  const double e1 = (h ? d3 : d1) + __shfl_xor_sync(0xffffffffu, h ? d1 : d3, 16);
+  double f = (b ? e1 : e0) + __shfl_xor_sync(0xffffffffu, b ? e0 : e1, 8);
+  f += __shfl_xor_sync(0xffffffffu, f, 4);
+  f += __shfl_xor_sync(0xffffffffu, f, 2);
+  f += __shfl_xor_sync(0xffffffffu, f, 1);
+  return __shfl_sync(0xffffffffu, f, (lane & 3) * 8);
+}
+
 // One row's lane partials: q = sum z^2 and ls = sum ln sigma (learned) over the lane's
-// elements. Row pointers are formed once, indices stay 32-bit.
+// elements, z = (x - mu) / sigma. Row pointers are formed once, indices stay 32-bit.
 template <typename T, bool VEC, int NQ>
 __device__ __forceinline__ void row_partials(const T* mu0, const float* x0, const float* ls0,
                                              const float* s_isig, int64_t base, int n, bool learned,
@@ -112,10 +129,9 @@ __device__ __forceinline__ void row_partials(const T* mu0, const float* x0, cons
           iv = *reinterpret_cast<const float4*>(s_isig + j);
         }
         // packed fp32x2 (FADD2 / FMUL2 / FFMA2): two elements per instruction
-        const float2 za = __fmul2_rn(__fadd2_rn(make_float2(xv.x, xv.y), make_float2(-m.x, -m.y)),
-                                     make_float2(iv.x, iv.y));
-        const float2 zb = __fmul2_rn(__fadd2_rn(make_float2(xv.z, xv.w), make_float2(-m.z, -m.w)),
-                                     make_float2(iv.z, iv.w));
+        const float2 ia = make_float2(iv.x, iv.y), ib = make_float2(iv.z, iv.w);
+        const float2 za = __fmul2_rn(__fadd2_rn(make_float2(xv.x, xv.y), make_float2(-m.x, -m.y)), ia);
+        const float2 zb = __fmul2_rn(__fadd2_rn(make_float2(xv.z, xv.w), make_float2(-m.z, -m.w)), ib);
         q2 = __ffma2_rn(za, za, __ffma2_rn(zb, zb, q2));
       }
     }
@@ -137,20 +153,24 @@ __device__ __forceinline__ void row_partials(const T* mu0, const float* x0, cons
   }
 }
 
-// dmu = g z / sigma, dln sigma = g (z^2 - 1) - c for one row (exact zeros when g = c = 0)
+// dmu = g (z / sigma), dln sigma = g (z^2 - 1) - c for one row (exact zeros when g = c = 0);
+// the row is read at `base` of mu0 / x0 / ls0 (global memory or a staged SMEM tile) and
+// written at `dbase` of dmu0 / dls0
 template <typename T, bool VEC, int NQ>
 __device__ __forceinline__ void row_backward(const T* mu0, const float* x0, const float* ls0, T* dmu0,
-                                             float* dls0, const float* s_isig, int64_t base, int n,
-                                             bool learned, int lane, float g, float c) {
+                                             float* dls0, const float* s_isig, int64_t base,
+                                             int64_t dbase, int n, bool learned, int lane, float g,
+                                             float c) {
   const bool active = g != 0.f || c != 0.f;
   const T* mu = mu0 + base;
   const float* x = x0 + base;
   const float* lsd = learned ? ls0 + base : nullptr;
-  T* dmu = dmu0 ? dmu0 + base : nullptr;
-  float* dls = dls0 ? dls0 + base : nullptr;
+  T* dmu = dmu0 ? dmu0 + dbase : nullptr;
+  float* dls = dls0 ? dls0 + dbase : nullptr;
   if (VEC) {
     constexpr int kIters = NQ > 0 ? (NQ + 31) / 32 : 1;
     const int nq = NQ > 0 ? NQ : (n >> 2);
+    const float2 g2 = make_float2(g, g);
 #pragma unroll
     for (int it = 0; it < kIters; ++it)
     for (int gi = lane + 32 * it; gi < nq; gi += (NQ > 0 ? nq : 32)) {
@@ -169,13 +189,12 @@ __device__ __forceinline__ void row_backward(const T* mu0, const float* x0, cons
         const float2 ia = make_float2(iv.x, iv.y), ib = make_float2(iv.z, iv.w);
         const float2 za = __fmul2_rn(__fadd2_rn(make_float2(xv.x, xv.y), make_float2(-m.x, -m.y)), ia);
         const float2 zb = __fmul2_rn(__fadd2_rn(make_float2(xv.z, xv.w), make_float2(-m.z, -m.w)), ib);
-        const float2 g2 = make_float2(g, g);
-        const float2 da = __fmul2_rn(__fmul2_rn(g2, za), ia), db = __fmul2_rn(__fmul2_rn(g2, zb), ib);
+        const float2 wa = __fmul2_rn(za, ia), wb = __fmul2_rn(zb, ib);
+        const float2 da = __fmul2_rn(g2, wa), db = __fmul2_rn(g2, wb);
         dm = make_float4(da.x, da.y, db.x, db.y);
-        const float z0 = za.x, z1 = za.y, z2 = zb.x, z3 = zb.y;
         if (dls)
-          dl = make_float4(fmaf(g, fmaf(z0, z0, -1.f), -c), fmaf(g, fmaf(z1, z1, -1.f), -c),
-                           fmaf(g, fmaf(z2, z2, -1.f), -c), fmaf(g, fmaf(z3, z3, -1.f), -c));
+          dl = make_float4(fmaf(g, fmaf(za.x, za.x, -1.f), -c), fmaf(g, fmaf(za.y, za.y, -1.f), -c),
+                           fmaf(g, fmaf(zb.x, zb.x, -1.f), -c), fmaf(g, fmaf(zb.y, zb.y, -1.f), -c));
       }
       if (dmu) st_mu4<T>(dmu, j, dm);
       if (dls) *reinterpret_cast<float4*>(dls + j) = dl;
@@ -188,55 +207,43 @@ __device__ __forceinline__ void row_backward(const T* mu0, const float* x0, cons
         iv = learned ? __expf(-lsd[j]) : s_isig[j];
         zz = (x[j] - m) * iv;
       }
-      if (dmu) st_mu<T>(dmu, j, active ? g * zz * iv : 0.f);
+      if (dmu) st_mu<T>(dmu, j, active ? g * (zz * iv) : 0.f);
       if (dls) dls[j] = active ? fmaf(g, fmaf(zz, zz, -1.f), -c) : 0.f;
     }
   }
 }
 
-// MODE 0: forward only, 1: fused PPO, 2: external backward (grad_logp given).
-// A warp takes tiles of kTile rows. Pass 1: row by row, coalesced element-parallel loads,
-// each lane's partial sums parked in SMEM [row][lane]. Epilogue: lane t owns row t of the
-// tile: it sums the 32 partials in fixed order in fp64, forms logp / H and runs the PPO
-// epilogue (its metadata loads are coalesced across lanes) — the per-row scalar work is
-// spread over the lanes instead of repeated by all 32. Pass 2: row by row, g and c are
-// broadcast and the backward re-reads the row (L1/L2) to write dmu / dln sigma.
-// VEC: 4-wide vector loads (n % 4 == 0, aligned pointers); otherwise scalar loops.
-#ifndef RLVLA_FLOW_MINB
-#define RLVLA_FLOW_MINB 4  // resident CTAs per SM the register budget is sized for
-#endif
-template <typename T, int MODE, bool VEC, int NQ>
-__global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(FlowArgs a) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int K = a.c.n_steps, D = a.c.dim, n = NQ > 0 ? 4 * NQ : K * D;
-  const bool learned = a.c.log_std != nullptr;
-  const bool want_stats = a.stats != nullptr && MODE != 2;
-  // the row arrays in registers once (not re-read from the parameter bank per row)
-  const T* const mu0 = static_cast<const T*>(a.c.mu);
-  const float* const x0 = a.c.x;
-  const float* const ls0 = a.c.log_std;
-  T* const dmu0 = static_cast<T*>(a.dmu);
-  float* const dls0 = a.dlog_std;
-  extern __shared__ __align__(16) float dsm[];
-  float* s_isig = dsm;                                        // [n] (sigma schedule)
-  float* pq = dsm + ((n + 3) & ~3) + warp * 2 * kTile * kPad;  // [kTile][kPad] per warp
-  float* pl = pq + kTile * kPad;
-  __shared__ double s_lnsig;
-  // sigma schedule: 1/sigma per element (no division or k = j / D in the loops) and
-  // D sum_k ln sigma_k in fp64, once per CTA
-  if (!learned) {
-    for (int j = threadIdx.x; j < n; j += blockDim.x) s_isig[j] = 1.f / a.c.sigma_k[j / D];
+// Per-CTA constants of one launch (the sigma schedule's 1/sigma table lives in SMEM)
+struct FlowCtx {
+  PpoConst pc;
+  double Nden, cst, lnsig;
+  const float* s_isig;
+  int n;
+  bool learned, want_stats;
+};
+
+template <int MODE>
+__device__ __forceinline__ FlowCtx flow_setup(const FlowArgs& a, int n, float* s_isig, int table,
+                                              double* s_lnsig) {
+  FlowCtx x{};
+  const int K = a.c.n_steps, D = a.c.dim;
+  x.n = n;
+  x.learned = a.c.log_std != nullptr;
+  x.want_stats = a.stats != nullptr && MODE != 2;
+  x.s_isig = s_isig;
+  // sigma schedule: 1/sigma per element of `table` = n (a row) or 4n (a tile's rows) — no
+  // division or k = j / D in the loops — and D sum_k ln sigma_k in fp64, once per CTA
+  if (!x.learned) {
+    for (int j = threadIdx.x; j < table; j += blockDim.x) s_isig[j] = 1.f / a.c.sigma_k[(j % n) / D];
     if (threadIdx.x == 0) {
       double acc = 0.0;
       for (int k = 0; k < K; ++k) acc += log(double(a.c.sigma_k[k]));
-      s_lnsig = acc * double(D);
+      *s_lnsig = acc * double(D);
     }
   }
-  __syncthreads();
-  const double cst = 0.5 * 1.8378770664093453 * double(n);  // n ln(2 pi) / 2
-  PpoConst pc{};
-  double Nden = 0.0;
+  x.cst = 0.5 * 1.8378770664093453 * double(n);  // n ln(2 pi) / 2
   if (MODE == 1) {
+    PpoConst& pc = x.pc;
     pc.has_prox = a.f.logp_prox != nullptr;
     pc.has_ref = a.f.logp_ref != nullptr && a.f.kl_coef != 0.f;
     pc.cur_version = a.f.cur_version;
@@ -247,92 +254,239 @@ __global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(
     pc.dual_clip = a.f.dual_clip;
     pc.kl_coef = a.f.kl_coef;
     pc.ent_coef = a.f.ent_coef;
-    Nden = loss_denominator(a.f.tok_denominator, a.f.adv_stats);
-    pc.invN = Nden > 0.0 ? float(1.0 / Nden) : 0.f;
+    x.Nden = loss_denominator(a.f.tok_denominator, a.f.adv_stats);
+    pc.invN = x.Nden > 0.0 ? float(1.0 / x.Nden) : 0.f;
   }
-  // per-lane statistics of the few rows this lane owns in fp32 (deterministic order); the
-  // warp, CTA and grid reductions are fp64
-  float acc[kLossSlots] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  const int64_t ntiles = (a.c.rows + kTile - 1) / kTile;
-  const int64_t gw = int64_t(blockIdx.x) * kFlowWarps + warp, nw = int64_t(gridDim.x) * kFlowWarps;
-  for (int64_t tile = gw; tile < ntiles; tile += nw) {
-    const int64_t r0 = tile * kTile;
-    const int nt = int(a.c.rows - r0 < kTile ? a.c.rows - r0 : kTile);
-    const int64_t r = r0 + lane;  // the row whose epilogue this lane runs (lane < nt)
-    // epilogue inputs first: their (coalesced) loads overlap pass 1
-    RowMeta4 mt;
-    float gin = 0.f;
-    if (lane < nt) {
-      if (MODE == 1) {
-        mt.lpb = a.f.logp_behav[r];
-        mt.lpp = a.f.logp_prox ? a.f.logp_prox[r] : 0.f;
-        mt.lref = pc.has_ref ? a.f.logp_ref[r] : 0.f;
-        mt.adv = a.f.adv[r];
-        mt.ver = a.f.version[r];
-        mt.valid = a.f.slot_key[r] != 0ull;
-      } else if (MODE == 2) {
-        gin = a.grad_logp[r];
-      }
+  return x;
+}
+
+// MODE 0: forward only, 1: fused PPO, 2: external backward (grad_logp given).
+// A warp tile is rows r0 .. r0+nt-1 (nt <= 4). Its PPO inputs are loaded first (coalesced, one
+// row per lane; no branch: lanes >= nt re-load row r0, so that no reconvergence point forces the
+// loads to complete before pass 1 has run)
+template <int MODE>
+__device__ __forceinline__ RowMeta4 load_meta(const FlowArgs& a, const FlowCtx& x, int64_t r0,
+                                              int nt, int lane, float& gin) {
+  const int64_t rl = lane < nt ? r0 + lane : r0;
+  RowMeta4 mt;
+  gin = 0.f;
+  if (MODE == 1) {
+    mt.lpb = a.f.logp_behav[rl];
+    mt.lpp = a.f.logp_prox ? a.f.logp_prox[rl] : 0.f;
+    mt.lref = x.pc.has_ref ? a.f.logp_ref[rl] : 0.f;
+    mt.adv = a.f.adv[rl];
+    mt.ver = a.f.version[rl];
+    mt.key = a.f.slot_key[rl];
+  } else if (MODE == 2) {
+    gin = a.grad_logp[rl];
+  }
+  return mt;
+}
+
+// Epilogue: lane t < nt owns row t, whose fp64 totals row_totals4 left there: logp / H and the
+// PPO epilogue — the per-row scalar work spread over the lanes instead of repeated by all 32.
+// Returns the row's g = dL/dlogp and c (entropy term); acc: the lane's fp32 statistics.
+template <int MODE>
+__device__ __forceinline__ void tile_epilogue(const FlowArgs& a, const FlowCtx& x, const RowMeta4& mt,
+                                              double qd, double ld, int n, int64_t r0, int nt,
+                                              int lane, float* acc, float& g, float& c) {
+  g = c = 0.f;
+  if (lane >= nt) return;
+  const int64_t r = r0 + lane;
+  const double lnsig = x.learned ? ld : x.lnsig;
+  const float logp = float(-0.5 * qd - lnsig - x.cst);
+  const float H = float(lnsig + x.cst + 0.5 * double(n));
+  PpoRowIn in;
+  in.tgt_status = isfinite(logp) ? 0 : 3;
+  in.logp = logp;
+  in.H = H;
+  RowStats rs;
+  float lt = 0.f;
+  if (MODE == 1) {
+    in.lpb = mt.lpb;
+    in.lpp = mt.lpp;
+    in.lref = mt.lref;
+    in.adv = mt.adv;
+    in.ver = mt.ver;
+    in.valid = mt.key != 0ull;
+    PpoMid t;
+    g = ppo_grad(x.pc, in, t);
+    c = t.m ? x.pc.ent_coef * x.pc.invN : 0.f;
+    ppo_stats(x.pc, in, t, rs, &lt);
+    if (a.f.out_grad_logp) a.f.out_grad_logp[r] = g;
+    if (a.f.out_loss_tok) a.f.out_loss_tok[r] = lt;
+  } else {
+    fwd_row_stats(in, rs);
+  }
+  if (a.logp) a.logp[r] = logp;
+  if (x.want_stats) acc_stats_f(acc, rs);
+}
+
+// Row-by-row tile (any shape): read at element offset `sbase` of mu_s / x_s / ls_s (the global
+// arrays, or a staged SMEM copy of the tile at sbase 0), written at the rows' global offsets.
+// Pass 1: coalesced element-parallel loads, the lane partials of all four rows in registers.
+// Pass 2: g and c are broadcast row by row and the backward re-reads the row.
+// VEC: 4-wide vector loads (n % 4 == 0, aligned pointers); otherwise scalar loops.
+template <typename T, int MODE, bool VEC, int NQ>
+__device__ __forceinline__ void flow_tile(const FlowArgs& a, const FlowCtx& x, const T* mu_s,
+                                          const float* x_s, const float* ls_s, int64_t sbase,
+                                          int64_t r0, int nt, float* acc, int lane) {
+  const int n = NQ > 0 ? 4 * NQ : x.n;
+  const bool learned = x.learned;
+  float gin;
+  const RowMeta4 mt = load_meta<MODE>(a, x, r0, nt, lane, gin);
+  float g = gin, c = 0.f;
+  if (MODE != 2) {
+    float q[kTile], l[kTile];
+#pragma unroll
+    for (int t = 0; t < kTile; ++t) {  // pass 1: each lane's partials of the four rows
+      q[t] = l[t] = 0.f;
+      if (t < nt)
+        row_partials<T, VEC, NQ>(mu_s, x_s, ls_s, x.s_isig, sbase + int64_t(t) * n, n, learned, lane,
+                                 q[t], l[t]);
     }
-    float g = 0.f, c = 0.f;
-    if (MODE != 2) {
+    const double qd = row_totals4(q, lane);
+    const double ld = learned ? row_totals4(l, lane) : 0.0;
+    tile_epilogue<MODE>(a, x, mt, qd, ld, n, r0, nt, lane, acc, g, c);
+  }
+  if (MODE != 0 && (a.dmu != nullptr || a.dlog_std != nullptr)) {
 #pragma unroll 2
-      for (int t = 0; t < nt; ++t) {  // pass 1: lane partials of each row -> SMEM
-        float q, ls;
-        row_partials<T, VEC, NQ>(mu0, x0, ls0, s_isig, (r0 + t) * n, n, learned, lane, q, ls);
-        pq[t * kPad + lane] = q;
-        if (learned) pl[t * kPad + lane] = ls;
-      }
-      __syncwarp();
-      if (lane < nt) {
-        double qd = 0.0, ld = 0.0;
-        for (int l = 0; l < 32; ++l) {  // fixed order, fp64
-          qd += double(pq[lane * kPad + l]);
-          if (learned) ld += double(pl[lane * kPad + l]);
-        }
-        const double lnsig = learned ? ld : s_lnsig;
-        const float logp = float(-0.5 * qd - lnsig - cst);
-        const float H = float(lnsig + cst + 0.5 * double(n));
-        PpoRowIn in;
-        in.tgt_status = isfinite(logp) ? 0 : 3;
-        in.logp = logp;
-        in.H = H;
-        RowStats rs;
-        float lt = 0.f;
-        if (MODE == 1) {
-          in.lpb = mt.lpb;
-          in.lpp = mt.lpp;
-          in.lref = mt.lref;
-          in.adv = mt.adv;
-          in.ver = mt.ver;
-          in.valid = mt.valid;
-          PpoMid t;
-          g = ppo_grad(pc, in, t);
-          c = t.m ? pc.ent_coef * pc.invN : 0.f;
-          ppo_stats(pc, in, t, rs, &lt);
-          if (a.f.out_grad_logp) a.f.out_grad_logp[r] = g;
-          if (a.f.out_loss_tok) a.f.out_loss_tok[r] = lt;
+    for (int t = 0; t < nt; ++t) {  // pass 2 (the rows were just read: SMEM, L1 or L2)
+      const float gt = __shfl_sync(0xffffffffu, g, t);
+      const float ct = __shfl_sync(0xffffffffu, c, t);
+      row_backward<T, VEC, NQ>(mu_s, x_s, ls_s, static_cast<T*>(a.dmu), a.dlog_std, x.s_isig,
+                               sbase + int64_t(t) * n, (r0 + t) * n, n, learned, lane, gt, ct);
+    }
+  }
+}
+
+// Flat tile (a full, staged tile of the paper's shapes; MODE 0 or 1): the tile's four rows are
+// contiguous in the stage and in dmu / dln sigma, so both passes walk its kTile NQ quads
+// lane-strided as one array — no per-row loop tails. A 32-quad step spans at most two rows
+// (NQ >= 32), so the row of a quad is a compile-time constant or one compare. Pass 1 leaves what
+// the backward needs in place of x (and ln sigma): w = z / sigma for a sigma schedule, z and
+// 1/sigma when learned (each lane rewrites only the quads it read), so pass 2 is a load, a
+// multiply and a store per element. s_isig holds the tile's 4n elements; mt: the tile's PPO
+// inputs, loaded by the caller a tile ahead (their latency under a saturated HBM exceeds a pass).
+template <typename T, int MODE, int NQ, bool LEARNED>
+__device__ __forceinline__ void flow_tile_flat(const FlowArgs& a, const FlowCtx& x, const T* mu_s,
+                                               float* x_s, float* ls_s, int64_t r0,
+                                               const RowMeta4& mt, float* acc, int lane) {
+  static_assert(NQ >= 32 && MODE != 2, "flat tiles: rows of >= 128 elements, a pass 1");
+  constexpr int n = 4 * NQ, kQ = kTile * NQ, kIt = (kQ + 31) / 32;
+  float2 q2[kTile];
+  float l[kTile];
+#pragma unroll
+  for (int t = 0; t < kTile; ++t) {
+    q2[t] = make_float2(0.f, 0.f);
+    l[t] = 0.f;
+  }
+#pragma unroll
+  for (int i = 0; i < kIt; ++i) {  // pass 1
+    const int qd = lane + 32 * i;
+    if ((i + 1) * 32 <= kQ || qd < kQ) {
+      const int j = 4 * qd;
+      const float4 m = ld_mu4<T>(mu_s, j);
+      const float4 xv = *reinterpret_cast<const float4*>(x_s + j);
+      float4 iv;
+      if (LEARNED) {
+        const float4 lv = *reinterpret_cast<const float4*>(ls_s + j);
+        iv = make_float4(__expf(-lv.x), __expf(-lv.y), __expf(-lv.z), __expf(-lv.w));
+        const float ls = (lv.x + lv.y) + (lv.z + lv.w);
+        const int lo = (32 * i) / NQ, hi = (32 * i + 31) / NQ < kTile ? (32 * i + 31) / NQ : kTile - 1;
+        if (lo == hi) {
+          l[lo] += ls;
         } else {
-          fwd_row_stats(in, rs);
+          const bool up = qd >= hi * NQ;
+          l[lo] += up ? 0.f : ls;
+          l[hi] += up ? ls : 0.f;
         }
-        if (a.logp) a.logp[r] = logp;
-        if (want_stats) acc_stats_f(acc, rs);
+      } else {
+        iv = *reinterpret_cast<const float4*>(x.s_isig + j);
       }
-      __syncwarp();  // the partials are read before the next tile overwrites them
-    } else {
-      g = gin;
-    }
-    if (MODE != 0 && (a.dmu != nullptr || a.dlog_std != nullptr)) {
-#pragma unroll 2
-      for (int t = 0; t < nt; ++t) {  // pass 2 (the rows were just read: L1/L2 hits)
-        const float gt = __shfl_sync(0xffffffffu, g, t);
-        const float ct = __shfl_sync(0xffffffffu, c, t);
-        row_backward<T, VEC, NQ>(mu0, x0, ls0, dmu0, dls0, s_isig, (r0 + t) * n, n, learned, lane, gt, ct);
+      const float2 ia = make_float2(iv.x, iv.y), ib = make_float2(iv.z, iv.w);
+      const float2 za = __fmul2_rn(__fadd2_rn(make_float2(xv.x, xv.y), make_float2(-m.x, -m.y)), ia);
+      const float2 zb = __fmul2_rn(__fadd2_rn(make_float2(xv.z, xv.w), make_float2(-m.z, -m.w)), ib);
+      const int lo = (32 * i) / NQ, hi = (32 * i + 31) / NQ < kTile ? (32 * i + 31) / NQ : kTile - 1;
+      if (lo == hi) {
+        q2[lo] = __ffma2_rn(za, za, __ffma2_rn(zb, zb, q2[lo]));
+      } else {
+        const bool up = qd >= hi * NQ;
+        const float2 sl = __ffma2_rn(za, za, __ffma2_rn(zb, zb, q2[lo]));
+        const float2 sh = __ffma2_rn(za, za, __ffma2_rn(zb, zb, q2[hi]));
+        q2[lo] = up ? q2[lo] : sl;
+        q2[hi] = up ? sh : q2[hi];
+      }
+      if (MODE == 1) {
+        if (LEARNED) {
+          *reinterpret_cast<float4*>(x_s + j) = make_float4(za.x, za.y, zb.x, zb.y);
+          *reinterpret_cast<float4*>(ls_s + j) = iv;
+        } else {
+          const float2 wa = __fmul2_rn(za, ia), wb = __fmul2_rn(zb, ib);
+          *reinterpret_cast<float4*>(x_s + j) = make_float4(wa.x, wa.y, wb.x, wb.y);
+        }
       }
     }
   }
-  if (!want_stats) return;
-  __shared__ double red[kFlowWarps][kLossSlots];
+  float q[kTile];
+#pragma unroll
+  for (int t = 0; t < kTile; ++t) q[t] = q2[t].x + q2[t].y;
+  const double qd = row_totals4(q, lane);
+  const double ld = LEARNED ? row_totals4(l, lane) : 0.0;
+  float g, c;
+  tile_epilogue<MODE>(a, x, mt, qd, ld, n, r0, kTile, lane, acc, g, c);
+  if (MODE == 0 || (a.dmu == nullptr && a.dlog_std == nullptr)) return;
+  __syncwarp();
+  float gt[kTile], ct[kTile];
+  bool all_active = true;
+#pragma unroll
+  for (int t = 0; t < kTile; ++t) {
+    gt[t] = __shfl_sync(0xffffffffu, g, t);
+    ct[t] = LEARNED ? __shfl_sync(0xffffffffu, c, t) : 0.f;
+    all_active = all_active && (gt[t] != 0.f || ct[t] != 0.f);
+  }
+  T* const dmu = a.dmu ? static_cast<T*>(a.dmu) + r0 * n : nullptr;
+  float* const dls = LEARNED && a.dlog_std ? a.dlog_std + r0 * n : nullptr;
+#pragma unroll
+  for (int i = 0; i < kIt; ++i) {  // pass 2
+    const int qd = lane + 32 * i;
+    if ((i + 1) * 32 <= kQ || qd < kQ) {
+      const int j = 4 * qd;
+      const int lo = (32 * i) / NQ, hi = (32 * i + 31) / NQ < kTile ? (32 * i + 31) / NQ : kTile - 1;
+      const bool up = lo != hi && qd >= hi * NQ;
+      const float gq = up ? gt[hi] : gt[lo];
+      const float cq = up ? ct[hi] : ct[lo];
+      const float2 g2 = make_float2(gq, gq);
+      float4 dm, dl = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (LEARNED) {
+        const float4 z = *reinterpret_cast<const float4*>(x_s + j);
+        const float4 iv = *reinterpret_cast<const float4*>(ls_s + j);
+        const float2 da = __fmul2_rn(g2, __fmul2_rn(make_float2(z.x, z.y), make_float2(iv.x, iv.y)));
+        const float2 db = __fmul2_rn(g2, __fmul2_rn(make_float2(z.z, z.w), make_float2(iv.z, iv.w)));
+        dm = make_float4(da.x, da.y, db.x, db.y);
+        dl = make_float4(fmaf(gq, fmaf(z.x, z.x, -1.f), -cq), fmaf(gq, fmaf(z.y, z.y, -1.f), -cq),
+                         fmaf(gq, fmaf(z.z, z.z, -1.f), -cq), fmaf(gq, fmaf(z.w, z.w, -1.f), -cq));
+      } else {
+        const float4 w = *reinterpret_cast<const float4*>(x_s + j);
+        const float2 da = __fmul2_rn(g2, make_float2(w.x, w.y));
+        const float2 db = __fmul2_rn(g2, make_float2(w.z, w.w));
+        dm = make_float4(da.x, da.y, db.x, db.y);
+      }
+      if (!all_active && gq == 0.f && cq == 0.f) {  // masked row: exact zeros
+        dm = make_float4(0.f, 0.f, 0.f, 0.f);
+        dl = dm;
+      }
+      if (dmu) st_mu4<T>(dmu, j, dm);
+      if (dls) *reinterpret_cast<float4*>(dls + j) = dl;
+    }
+  }
+}
+
+// The CTA's statistics: warp sums in fp64, then the warps in fixed order, then the grid
+template <int MODE, int WARPS>
+__device__ __forceinline__ void flow_finish(const FlowArgs& a, const FlowCtx& x, const float* acc,
+                                            int warp, int lane) {
+  __shared__ double red[WARPS][kLossSlots];
   __shared__ double cta[kLossSlots];
   double accd[kLossSlots];
   for (int k = 0; k < kLossSlots; ++k) accd[k] = warp_sum_d(double(acc[k]));
@@ -341,15 +495,144 @@ __global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(
   __syncthreads();
   if (threadIdx.x < kLossSlots) {
     double sm = 0;
-    for (int w = 0; w < kFlowWarps; ++w) sm += red[w][threadIdx.x];
+    for (int w = 0; w < WARPS; ++w) sm += red[w][threadIdx.x];
     cta[threadIdx.x] = sm;
   }
   __syncthreads();
-  finish_loss_stats(cta, a.stats, a.ws.partials, a.ws.ctrl + CTRL_FLOW, Nden,
+  finish_loss_stats(cta, a.stats, a.ws.partials, a.ws.ctrl + CTRL_FLOW, x.Nden,
                     MODE == 1 ? a.f.accumulate : 0, MODE == 1 ? a.f.ent_coef : 0.f, &a.ws.p2p);
 }
 
-size_t flow_smem(int n) { return size_t((n + 3) & ~3) * 4 + size_t(kFlowWarps) * 2 * kTile * kPad * 4; }
+#ifndef RLVLA_FLOW_MINB
+#define RLVLA_FLOW_MINB 4  // resident CTAs per SM the register budget is sized for
+#endif
+// Direct-load kernel: any row length, rows streamed straight from global memory.
+template <typename T, int MODE, bool VEC, int NQ>
+__global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(FlowArgs a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = NQ > 0 ? 4 * NQ : a.c.n_steps * a.c.dim;
+  extern __shared__ __align__(16) float dsm[];  // [n] 1/sigma (sigma schedule)
+  __shared__ double s_lnsig;
+  FlowCtx x = flow_setup<MODE>(a, n, dsm, n, &s_lnsig);
+  __syncthreads();
+  x.lnsig = s_lnsig;
+  // per-lane statistics of the few rows this lane owns in fp32 (deterministic order); the
+  // warp, CTA and grid reductions are fp64
+  float acc[kLossSlots] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const int64_t ntiles = (a.c.rows + kTile - 1) / kTile;
+  const int64_t gw = int64_t(blockIdx.x) * kFlowWarps + warp, nw = int64_t(gridDim.x) * kFlowWarps;
+  for (int64_t tile = gw; tile < ntiles; tile += nw) {
+    const int64_t r0 = tile * kTile;
+    const int nt = int(a.c.rows - r0 < kTile ? a.c.rows - r0 : kTile);
+    flow_tile<T, MODE, VEC, NQ>(a, x, static_cast<const T*>(a.c.mu), a.c.x, a.c.log_std, r0 * n, r0,
+                                nt, acc, lane);
+  }
+  if (!x.want_stats) return;
+  flow_finish<MODE, kFlowWarps>(a, x, acc, warp, lane);
+}
+
+// TMA-staged kernel for the paper's compile-time row lengths (NQ > 0, 16-byte aligned arrays):
+// every warp runs its own ring of kFlowStages tile buffers in SMEM, filled by 1-D bulk copies
+// (one per array per tile, mbarrier tx completion, L2 evict_first) that lane 0 issues
+// kFlowStages tiles ahead, so the HBM reads of the next tiles are in flight while the warp
+// computes on the current one; flow_tile_flat then works on the stage (MODE 2, which has no
+// pass 1, takes the row-by-row tile on it). The last, partial tile (rows % 4) is read directly
+// by the one warp that owns it.
+// warps per CTA: 8 with a sigma schedule (2 CTAs per SM fit), 4 with learned ln sigma (its
+// stages are twice the size: 2 CTAs of 4 measured faster than 1 of 8 — profiles/r1/FLOW.md)
+#ifndef RLVLA_FLOW_TMA_WARPS
+#define RLVLA_FLOW_TMA_WARPS 8
+#endif
+#ifndef RLVLA_FLOW_TMA_WARPS_LEARNED
+#define RLVLA_FLOW_TMA_WARPS_LEARNED 4
+#endif
+#ifndef RLVLA_FLOW_STAGES
+#define RLVLA_FLOW_STAGES 2
+#endif
+template <bool LEARNED>
+constexpr int tma_warps() {
+  return LEARNED ? RLVLA_FLOW_TMA_WARPS_LEARNED : RLVLA_FLOW_TMA_WARPS;
+}
+constexpr int kFlowStages = RLVLA_FLOW_STAGES;
+
+template <typename T, int NQ>
+__host__ __device__ constexpr int tma_stage_bytes(bool learned) {
+  return kTile * 4 * NQ * (int(sizeof(T)) + 4 + (learned ? 4 : 0));
+}
+// barriers, then the tile's 1/sigma table (4n floats), then the per-warp rings
+template <int NQ, int WARPS>
+__host__ __device__ constexpr int tma_ring_offset() {
+  return ((8 * WARPS * kFlowStages + 4 * kTile * 4 * NQ) + 127) & ~127;
+}
+
+template <typename T, int MODE, int NQ, bool LEARNED>
+__global__ void __launch_bounds__(tma_warps<LEARNED>() * 32) flow_tma_kernel(FlowArgs a) {
+  constexpr int kTmaWarps = tma_warps<LEARNED>();
+  constexpr int n = 4 * NQ;
+  constexpr int kMuB = kTile * n * int(sizeof(T)), kXB = kTile * n * 4;
+  constexpr int stage_b = tma_stage_bytes<T, NQ>(LEARNED);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  extern __shared__ __align__(128) unsigned char tsm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tsm) + warp * kFlowStages;  // [warp][stage]
+  float* s_isig = reinterpret_cast<float*>(tsm + 8 * kTmaWarps * kFlowStages);
+  unsigned char* ring = tsm + tma_ring_offset<NQ, kTmaWarps>() + size_t(warp) * kFlowStages * stage_b;
+  __shared__ double s_lnsig;
+  FlowCtx x = flow_setup<MODE>(a, n, s_isig, kTile * n, &s_lnsig);
+  if (lane == 0) {
+    for (int st = 0; st < kFlowStages; ++st) mbar_init(&bars[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  x.lnsig = s_lnsig;
+  float acc[kLossSlots] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const int64_t nfull = a.c.rows / kTile;
+  const int64_t gw = int64_t(blockIdx.x) * kTmaWarps + warp, nw = int64_t(gridDim.x) * kTmaWarps;
+  const int64_t cnt = gw < nfull ? (nfull - gw + nw - 1) / nw : 0;  // this warp's full tiles
+  const T* const mu0 = static_cast<const T*>(a.c.mu);
+  const uint64_t pol = policy_evict_first();
+  auto issue = [&](int64_t i) {  // lane 0: tile gw + i nw -> stage i % kFlowStages
+    const int64_t e0 = (gw + i * nw) * kTile * n;
+    unsigned char* st = ring + (i % kFlowStages) * stage_b;
+    uint64_t* bar = &bars[i % kFlowStages];
+    mbar_arrive_expect_tx(bar, uint32_t(stage_b));
+    bulk_g2s(st, mu0 + e0, kMuB, bar, pol);
+    bulk_g2s(st + kMuB, a.c.x + e0, kXB, bar, pol);
+    if (LEARNED) bulk_g2s(st + kMuB + kXB, a.c.log_std + e0, kXB, bar, pol);
+  };
+  if (lane == 0)
+    for (int64_t i = 0; i < cnt && i < kFlowStages; ++i) issue(i);
+  float gin;
+  RowMeta4 mt_next = load_meta<MODE>(a, x, gw < nfull ? gw * kTile : 0, kTile, lane, gin);
+  for (int64_t i = 0; i < cnt; ++i) {
+    unsigned char* st = ring + (i % kFlowStages) * stage_b;
+    mbar_wait(&bars[i % kFlowStages], uint32_t((i / kFlowStages) & 1));
+    const int64_t r0 = (gw + i * nw) * kTile;
+    if constexpr (MODE == 2)
+      flow_tile<T, MODE, true, NQ>(a, x, reinterpret_cast<const T*>(st),
+                                   reinterpret_cast<const float*>(st + kMuB),
+                                   reinterpret_cast<const float*>(st + kMuB + kXB), 0, r0, kTile, acc,
+                                   lane);
+    else {
+      const RowMeta4 mt = mt_next;  // the next tile's inputs (the last tile re-loads its own)
+      mt_next = load_meta<MODE>(a, x, (gw + (i + 1 < cnt ? i + 1 : i) * nw) * kTile, kTile, lane, gin);
+      flow_tile_flat<T, MODE, NQ, LEARNED>(a, x, reinterpret_cast<const T*>(st),
+                                           reinterpret_cast<float*>(st + kMuB),
+                                           reinterpret_cast<float*>(st + kMuB + kXB), r0, mt, acc, lane);
+    }
+    // the stage's generic-proxy reads and rewrites are ordered before its next TMA fill
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0 && i + kFlowStages < cnt) issue(i + kFlowStages);
+  }
+  const int64_t tail = a.c.rows - nfull * kTile;
+  if (tail > 0 && gw == nfull % nw)
+    flow_tile<T, MODE, true, NQ>(a, x, mu0, a.c.x, a.c.log_std, nfull * kTile * n, nfull * kTile,
+                                 int(tail), acc, lane);
+  if (!x.want_stats) return;
+  flow_finish<MODE, kTmaWarps>(a, x, acc, warp, lane);
+}
+
+size_t flow_smem(int n) { return size_t((n + 3) & ~3) * 4; }
 
 // grid = all resident CTAs (occupancy of the instantiation), fewer for small problems
 template <typename T, int MODE, bool VEC, int NQ>
@@ -379,8 +662,51 @@ cudaError_t launch_m(const FlowArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// TMA-staged launch: CTAs of tma_warps() warps, as many as fit (SMEM-bound), fewer for small
+// problems
+template <typename T, int MODE, int NQ, bool LEARNED>
+cudaError_t launch_tma(const FlowArgs& a, cudaStream_t s) {
+  constexpr int kTmaWarps = tma_warps<LEARNED>();
+  const size_t smem = size_t(tma_ring_offset<NQ, kTmaWarps>()) +
+                      size_t(kTmaWarps) * kFlowStages * tma_stage_bytes<T, NQ>(LEARNED);
+  static size_t attr[kMaxDevices] = {};
+  const int dev = device_info().device;
+  size_t dummy = 0;
+  size_t& cached = (dev >= 0 && dev < kMaxDevices) ? attr[dev] : dummy;
+  if (smem > 48 * 1024 && cached < smem) {
+    cudaError_t e = cudaFuncSetAttribute(flow_tma_kernel<T, MODE, NQ, LEARNED>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    cached = smem;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_tma_kernel<T, MODE, NQ, LEARNED>,
+                                                                kTmaWarps * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t tiles = (a.c.rows + kTile - 1) / kTile;
+  int64_t grid = (tiles + kTmaWarps - 1) / kTmaWarps;
+  const int64_t cap = int64_t(device_info().sm_count) * per_sm;
+  if (grid > cap) grid = cap;
+  flow_tma_kernel<T, MODE, NQ, LEARNED><<<int(grid), kTmaWarps * 32, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+#ifndef RLVLA_FLOW_TMA
+#define RLVLA_FLOW_TMA 1  // 0: the paper's shapes take the direct kernel too (A/B)
+#endif
 template <typename T, bool VEC, int NQ>
 cudaError_t launch_q(const FlowArgs& a, cudaStream_t s) {
+  // bulk copies need 16-byte aligned tiles: the arrays' bases (a tile is a multiple of 16 B)
+  if constexpr (RLVLA_FLOW_TMA && VEC && NQ > 0) {
+    if (reinterpret_cast<uintptr_t>(a.c.mu) % 16 == 0 && reinterpret_cast<uintptr_t>(a.c.x) % 16 == 0 &&
+        (!a.c.log_std || reinterpret_cast<uintptr_t>(a.c.log_std) % 16 == 0)) {
+      const bool learned = a.c.log_std != nullptr;
+      if (a.grad_logp) return learned ? launch_tma<T, 2, NQ, true>(a, s) : launch_tma<T, 2, NQ, false>(a, s);
+      if (a.fused) return learned ? launch_tma<T, 1, NQ, true>(a, s) : launch_tma<T, 1, NQ, false>(a, s);
+      return learned ? launch_tma<T, 0, NQ, true>(a, s) : launch_tma<T, 0, NQ, false>(a, s);
+    }
+  }
   if (a.grad_logp) return launch_m<T, 2, VEC, NQ>(a, s);
   if (a.fused) return launch_m<T, 1, VEC, NQ>(a, s);
   return launch_m<T, 0, VEC, NQ>(a, s);
@@ -391,8 +717,10 @@ cudaError_t launch_q(const FlowArgs& a, cudaStream_t s) {
 template <typename T, bool VEC>
 cudaError_t launch_v(const FlowArgs& a, cudaStream_t s) {
   const int n = a.c.n_steps * a.c.dim;
-  if (VEC && n == 280) return launch_q<T, VEC, 70>(a, s);
-  if (VEC && n == 140) return launch_q<T, VEC, 35>(a, s);
+  if constexpr (VEC) {
+    if (n == 280) return launch_q<T, VEC, 70>(a, s);
+    if (n == 140) return launch_q<T, VEC, 35>(a, s);
+  }
   return launch_q<T, VEC, 0>(a, s);
 }
 

@@ -74,6 +74,29 @@ VARS = [dict(), dict(dual_clip=3.0, kl_coef=0.1), dict(ent_coef=0.01)]
 @pytest.mark.parametrize("learned", [False, True])
 @pytest.mark.parametrize("var", VARS)
 def test_fused_ppo(R, K, D, dtype, learned, var):
+    _run_fused(R, K, D, dtype, learned, var)
+
+
+@pytest.mark.parametrize("R,K,D", SHAPES[:2])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("learned", [False, True])
+def test_fused_ppo_unaligned(R, K, D, dtype, learned):
+    """Arrays 8 bytes off a 16-byte boundary: the paper's shapes then skip the TMA-staged kernel
+    (bulk copies need 16-byte aligned tiles) and run the direct one (bf16 4-wide, f32 scalar)."""
+    _run_fused(R, K, D, dtype, learned, {}, offset_bytes=8)
+
+
+def _offset(t, nbytes):
+    """A copy of t whose data pointer sits `nbytes` past a 256-byte aligned allocation."""
+    k = nbytes // t.element_size()
+    buf = torch.empty(t.numel() + k, dtype=t.dtype, device=t.device)
+    v = buf[k:].view(t.shape)
+    v.copy_(t)
+    assert v.data_ptr() % 16 == nbytes % 16
+    return v
+
+
+def _run_fused(R, K, D, dtype, learned, var, offset_bytes=0):
     P = _P()
     mu, mu64, x, ls = _case(R, K, D, dtype, learned, seed=1)
     o = F.chain_logprob(mu64, x, sigma_k=SIG_K[:K], log_std=ls)
@@ -91,10 +114,15 @@ def test_fused_ppo(R, K, D, dtype, learned, var):
     fa = P.ppo_args(logp_behav=cu(lb), adv=cu(adv), version=cu(ver), slot_key=cu(key), a_tok=1,
                     cur_version=100, tok_denominator=N, out_grad_logp=g, out_loss_tok=lt,
                     logp_ref=cu(lref) if var.get("kl_coef") else None, **var)
-    ch = P.GaussChain(mu.cuda(), cu(x), cu(SIG_K[:K]), None if ls is None else cu(ls))
-    logp = torch.empty(R, device="cuda")
-    dmu = torch.empty_like(ch.mu)
+    mu_d, x_d, ls_d = mu.cuda(), cu(x), None if ls is None else cu(ls)
+    dmu = torch.empty_like(mu_d)
     dls = torch.empty(R, K, D, device="cuda") if learned else None
+    if offset_bytes:
+        mu_d, x_d, dmu = _offset(mu_d, offset_bytes), _offset(x_d, offset_bytes), _offset(dmu, offset_bytes)
+        ls_d = None if ls_d is None else _offset(ls_d, offset_bytes)
+        dls = None if dls is None else _offset(dls, offset_bytes)
+    ch = P.GaussChain(mu_d, x_d, cu(SIG_K[:K]), ls_d)
+    logp = torch.empty(R, device="cuda")
     st = torch.zeros(24, dtype=torch.float64, device="cuda")
     P.rlvla_flow_logprob(ch, logp=logp, fused=fa, dmu=dmu, dlog_std=dls, stats=st, ws=P.workspace(1))
     # oracle: PPO over the chain log-probs, one token per decision step

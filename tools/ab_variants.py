@@ -12,10 +12,11 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
+    "l8": ("RLVLA_FLOW_TMA_WARPS_LEARNED=8",),
 }
 # name -> git revision whose csrc/ + include/ are built as one more variant
 # (the ABI only grew at the end of its structs, so today's binding drives older libraries)
-REVISIONS = {}  # e.g. {"prev": "HEAD"} builds the last commit as a variant
+REVISIONS = {"prev": "HEAD"}  # e.g. {"prev": "HEAD"} builds the last commit as a variant
 
 
 def build_revision(name, rev):
@@ -72,6 +73,7 @@ def run(mode="fused", rounds=3):
                 cmd = [sys.executable, os.path.join(ROOT, "tools", "prof_scatter.py")]
             elif mode == "flow":
                 cmd = [sys.executable, os.path.join(ROOT, "tools", "prof_flow.py"), "--rows", "196608"]
+                cmd += os.environ.get("FLOW_ARGS", "").split()  # e.g. "--learned --f32"
             else:
                 cmd = [sys.executable, os.path.join(ROOT, "tools", "prof_fused.py"), "--mode", mode,
                        "--iters", "12"]
