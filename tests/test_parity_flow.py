@@ -80,10 +80,13 @@ def test_fused_ppo(R, K, D, dtype, learned, var):
 @pytest.mark.parametrize("R,K,D", SHAPES[:2])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("learned", [False, True])
-def test_fused_ppo_unaligned(R, K, D, dtype, learned):
-    """Arrays 8 bytes off a 16-byte boundary: the paper's shapes then skip the TMA-staged kernel
-    (bulk copies need 16-byte aligned tiles) and run the direct one (bf16 4-wide, f32 scalar)."""
-    _run_fused(R, K, D, dtype, learned, {}, offset_bytes=8)
+@pytest.mark.parametrize("which", ["data", "meta"])
+def test_fused_ppo_unaligned(R, K, D, dtype, learned, which):
+    """Arrays 8 bytes off a 16-byte boundary. data: the paper's shapes then skip the TMA-staged
+    kernel (bulk copies need 16-byte aligned tiles) and run the direct one (bf16 4-wide, f32
+    scalar); meta: the staged kernel loads the PPO inputs from global memory instead."""
+    _run_fused(R, K, D, dtype, learned, dict(kl_coef=0.1) if which == "meta" else {},
+               offset_bytes=8, offset_what=which)
 
 
 def _offset(t, nbytes):
@@ -96,7 +99,7 @@ def _offset(t, nbytes):
     return v
 
 
-def _run_fused(R, K, D, dtype, learned, var, offset_bytes=0):
+def _run_fused(R, K, D, dtype, learned, var, offset_bytes=0, offset_what="data"):
     P = _P()
     mu, mu64, x, ls = _case(R, K, D, dtype, learned, seed=1)
     o = F.chain_logprob(mu64, x, sigma_k=SIG_K[:K], log_std=ls)
@@ -109,15 +112,18 @@ def _run_fused(R, K, D, dtype, learned, var, offset_bytes=0):
     key = np.where(rng.random(R) < 0.95, 5, 0).astype(np.int64)
     N = float(R)
     cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    cm = cu  # the PPO inputs
+    if offset_bytes and offset_what == "meta":
+        cm = lambda a: _offset(cu(a), offset_bytes)  # noqa: E731
     g = torch.empty(R, device="cuda")
     lt = torch.empty(R, device="cuda")
-    fa = P.ppo_args(logp_behav=cu(lb), adv=cu(adv), version=cu(ver), slot_key=cu(key), a_tok=1,
+    fa = P.ppo_args(logp_behav=cm(lb), adv=cm(adv), version=cm(ver), slot_key=cm(key), a_tok=1,
                     cur_version=100, tok_denominator=N, out_grad_logp=g, out_loss_tok=lt,
-                    logp_ref=cu(lref) if var.get("kl_coef") else None, **var)
+                    logp_ref=cm(lref) if var.get("kl_coef") else None, **var)
     mu_d, x_d, ls_d = mu.cuda(), cu(x), None if ls is None else cu(ls)
     dmu = torch.empty_like(mu_d)
     dls = torch.empty(R, K, D, device="cuda") if learned else None
-    if offset_bytes:
+    if offset_bytes and offset_what == "data":
         mu_d, x_d, dmu = _offset(mu_d, offset_bytes), _offset(x_d, offset_bytes), _offset(dmu, offset_bytes)
         ls_d = None if ls_d is None else _offset(ls_d, offset_bytes)
         dls = None if dls is None else _offset(dls, offset_bytes)

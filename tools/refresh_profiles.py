@@ -102,7 +102,7 @@ def main():
     if os.path.exists(pre + "_fprof.log"):
         shutil.copy(pre + "_fprof.log", os.path.join(prof, "prof_flow.jsonl"))
         out, m = raw(pre + "_flow.ncu-rep")
-        open(os.path.join(prof, "ncu_full_flow_raw.csv"), "w").write(out)
+        open(os.path.join(prof, "ncu_full_flow_tma_raw.csv"), "w").write(out)
         f = open(os.path.join(prof, "FLOW.md")).read()
         tab = ["| rows | K x D | mu | ln sigma | alg. bytes | median us | GB/s | % of 6548.8 |", "|---|---|---|---|---|---|---|---|"]
         for d in jl(pre + "_fprof.log"):
