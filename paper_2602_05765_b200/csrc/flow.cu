@@ -14,7 +14,7 @@
 //   pass 2  step by step, g and c are broadcast and the backward writes
 //           dmu = g (z / sigma),   dln sigma = g (z^2 - 1) - c     (c = ent_coef m / N)
 // Two kernels run this tile: flow_tma_kernel for the paper's K x D shapes (280, 140 elements;
-// each warp's tiles staged HBM -> SMEM by bulk copies kFlowStages tiles ahead, pass 1 leaving
+// each warp's tiles staged HBM -> SMEM by bulk copies one or two tiles ahead, pass 1 leaving
 // z / sigma in place for pass 2) and flow_kernel for any other shape (direct loads; rows whose
 // length is not a multiple of 4, or unaligned pointers, take scalar loops).
 // Bytes per row: n (|mu| + 4 [+ 4 ln sigma]) read, n |mu| [+ 4 n] written.
@@ -532,42 +532,34 @@ __global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(
 }
 
 // TMA-staged kernel for the paper's compile-time row lengths (NQ > 0, 16-byte aligned arrays):
-// every warp runs its own ring of kFlowStages tile buffers in SMEM, filled by 1-D bulk copies
+// every warp runs its own ring of STAGES tile buffers in SMEM, filled by 1-D bulk copies
 // (one per array per tile, mbarrier tx completion, L2 evict_first) that lane 0 issues
-// kFlowStages tiles ahead, so the HBM reads of the next tiles are in flight while the warp
+// STAGES tiles ahead, so the HBM reads of the next tiles are in flight while the warp
 // computes on the current one; flow_tile_flat then works on the stage (MODE 2, which has no
 // pass 1, takes the row-by-row tile on it). The last, partial tile (rows % 4) is read directly
 // by the one warp that owns it.
-// warps per CTA: 8 with a sigma schedule (2 CTAs per SM fit), 4 with learned ln sigma (its
-// stages are twice the size: 2 CTAs of 4 measured faster than 1 of 8 — profiles/r1/FLOW.md)
-#ifndef RLVLA_FLOW_TMA_WARPS
-#define RLVLA_FLOW_TMA_WARPS 8
+// CTA shapes (warps, ring stages per warp): 8 x 2 with a sigma schedule (2 CTAs per SM fit),
+// 4 x 2 with learned ln sigma (stages twice the size: 2 CTAs of 4 measured faster than 1 of 8),
+// and 16 x 1 for a sigma schedule with fewer than ~4 tiles per warp of the 8 x 2 grid (one
+// update of 24,576 steps: more, shallower warps finish the few tiles sooner) —
+// profiles/r1/FLOW.md
+#ifndef RLVLA_FLOW_SMALL_TILES
+#define RLVLA_FLOW_SMALL_TILES 9472  // tiles below which the 16 x 1 shape runs (0: never)
 #endif
-#ifndef RLVLA_FLOW_TMA_WARPS_LEARNED
-#define RLVLA_FLOW_TMA_WARPS_LEARNED 4
-#endif
-#ifndef RLVLA_FLOW_STAGES
-#define RLVLA_FLOW_STAGES 2
-#endif
-template <bool LEARNED>
-constexpr int tma_warps() {
-  return LEARNED ? RLVLA_FLOW_TMA_WARPS_LEARNED : RLVLA_FLOW_TMA_WARPS;
-}
-constexpr int kFlowStages = RLVLA_FLOW_STAGES;
 
 template <typename T, int NQ>
 __host__ __device__ constexpr int tma_stage_bytes(bool learned) {
   return kTile * 4 * NQ * (int(sizeof(T)) + 4 + (learned ? 4 : 0));
 }
 // barriers, then the tile's 1/sigma table (4n floats), then the per-warp rings
-template <int NQ, int WARPS>
+template <int NQ, int WARPS, int STAGES>
 __host__ __device__ constexpr int tma_ring_offset() {
-  return ((8 * WARPS * kFlowStages + 4 * kTile * 4 * NQ) + 127) & ~127;
+  return ((8 * WARPS * STAGES + 4 * kTile * 4 * NQ) + 127) & ~127;
 }
 
-template <typename T, int MODE, int NQ, bool LEARNED>
-__global__ void __launch_bounds__(tma_warps<LEARNED>() * 32) flow_tma_kernel(FlowArgs a) {
-  constexpr int kTmaWarps = tma_warps<LEARNED>();
+template <typename T, int MODE, int NQ, bool LEARNED, int WARPS, int STAGES>
+__global__ void __launch_bounds__(WARPS * 32) flow_tma_kernel(FlowArgs a) {
+  constexpr int kTmaWarps = WARPS, kFlowStages = STAGES;
   constexpr int n = 4 * NQ;
   constexpr int kMuB = kTile * n * int(sizeof(T)), kXB = kTile * n * 4;
   constexpr int stage_b = tma_stage_bytes<T, NQ>(LEARNED);
@@ -575,7 +567,7 @@ __global__ void __launch_bounds__(tma_warps<LEARNED>() * 32) flow_tma_kernel(Flo
   extern __shared__ __align__(128) unsigned char tsm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(tsm) + warp * kFlowStages;  // [warp][stage]
   float* s_isig = reinterpret_cast<float*>(tsm + 8 * kTmaWarps * kFlowStages);
-  unsigned char* ring = tsm + tma_ring_offset<NQ, kTmaWarps>() + size_t(warp) * kFlowStages * stage_b;
+  unsigned char* ring = tsm + tma_ring_offset<NQ, kTmaWarps, kFlowStages>() + size_t(warp) * kFlowStages * stage_b;
   __shared__ double s_lnsig;
   FlowCtx x = flow_setup<MODE>(a, n, s_isig, kTile * n, &s_lnsig);
   if (lane == 0) {
@@ -662,25 +654,25 @@ cudaError_t launch_m(const FlowArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// TMA-staged launch: CTAs of tma_warps() warps, as many as fit (SMEM-bound), fewer for small
+// TMA-staged launch: CTAs of WARPS warps, as many as fit (SMEM-bound), fewer for small
 // problems
-template <typename T, int MODE, int NQ, bool LEARNED>
+template <typename T, int MODE, int NQ, bool LEARNED, int WARPS, int STAGES>
 cudaError_t launch_tma(const FlowArgs& a, cudaStream_t s) {
-  constexpr int kTmaWarps = tma_warps<LEARNED>();
-  const size_t smem = size_t(tma_ring_offset<NQ, kTmaWarps>()) +
-                      size_t(kTmaWarps) * kFlowStages * tma_stage_bytes<T, NQ>(LEARNED);
+  constexpr int kTmaWarps = WARPS;
+  const size_t smem = size_t(tma_ring_offset<NQ, WARPS, STAGES>()) +
+                      size_t(WARPS) * STAGES * tma_stage_bytes<T, NQ>(LEARNED);
   static size_t attr[kMaxDevices] = {};
   const int dev = device_info().device;
   size_t dummy = 0;
   size_t& cached = (dev >= 0 && dev < kMaxDevices) ? attr[dev] : dummy;
   if (smem > 48 * 1024 && cached < smem) {
-    cudaError_t e = cudaFuncSetAttribute(flow_tma_kernel<T, MODE, NQ, LEARNED>,
+    cudaError_t e = cudaFuncSetAttribute(flow_tma_kernel<T, MODE, NQ, LEARNED, WARPS, STAGES>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     cached = smem;
   }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_tma_kernel<T, MODE, NQ, LEARNED>,
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_tma_kernel<T, MODE, NQ, LEARNED, WARPS, STAGES>,
                                                                 kTmaWarps * 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
@@ -688,8 +680,15 @@ cudaError_t launch_tma(const FlowArgs& a, cudaStream_t s) {
   int64_t grid = (tiles + kTmaWarps - 1) / kTmaWarps;
   const int64_t cap = int64_t(device_info().sm_count) * per_sm;
   if (grid > cap) grid = cap;
-  flow_tma_kernel<T, MODE, NQ, LEARNED><<<int(grid), kTmaWarps * 32, smem, s>>>(a);
+  flow_tma_kernel<T, MODE, NQ, LEARNED, WARPS, STAGES><<<int(grid), kTmaWarps * 32, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+template <typename T, int NQ, bool LEARNED, int WARPS, int STAGES>
+cudaError_t launch_tma_m(const FlowArgs& a, cudaStream_t s, int mode) {
+  if (mode == 2) return launch_tma<T, 2, NQ, LEARNED, WARPS, STAGES>(a, s);
+  if (mode == 1) return launch_tma<T, 1, NQ, LEARNED, WARPS, STAGES>(a, s);
+  return launch_tma<T, 0, NQ, LEARNED, WARPS, STAGES>(a, s);
 }
 
 #ifndef RLVLA_FLOW_TMA
@@ -701,10 +700,10 @@ cudaError_t launch_q(const FlowArgs& a, cudaStream_t s) {
   if constexpr (RLVLA_FLOW_TMA && VEC && NQ > 0) {
     if (reinterpret_cast<uintptr_t>(a.c.mu) % 16 == 0 && reinterpret_cast<uintptr_t>(a.c.x) % 16 == 0 &&
         (!a.c.log_std || reinterpret_cast<uintptr_t>(a.c.log_std) % 16 == 0)) {
-      const bool learned = a.c.log_std != nullptr;
-      if (a.grad_logp) return learned ? launch_tma<T, 2, NQ, true>(a, s) : launch_tma<T, 2, NQ, false>(a, s);
-      if (a.fused) return learned ? launch_tma<T, 1, NQ, true>(a, s) : launch_tma<T, 1, NQ, false>(a, s);
-      return learned ? launch_tma<T, 0, NQ, true>(a, s) : launch_tma<T, 0, NQ, false>(a, s);
+      const int mode = a.grad_logp ? 2 : a.fused ? 1 : 0;
+      if (a.c.log_std != nullptr) return launch_tma_m<T, NQ, true, 4, 2>(a, s, mode);
+      if ((a.c.rows + kTile - 1) / kTile < RLVLA_FLOW_SMALL_TILES) return launch_tma_m<T, NQ, false, 16, 1>(a, s, mode);
+      return launch_tma_m<T, NQ, false, 8, 2>(a, s, mode);
     }
   }
   if (a.grad_logp) return launch_m<T, 2, VEC, NQ>(a, s);

@@ -12,10 +12,11 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
+    "nosmall": ("RLVLA_FLOW_SMALL_TILES=0",),
 }
 # name -> git revision whose csrc/ + include/ are built as one more variant
 # (the ABI only grew at the end of its structs, so today's binding drives older libraries)
-REVISIONS = {"prev": "HEAD"}  # e.g. {"prev": "HEAD"} builds the last commit as a variant
+REVISIONS = {}  # e.g. {"prev": "HEAD"} builds the last commit as a variant
 
 
 def build_revision(name, rev):
