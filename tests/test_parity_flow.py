@@ -27,7 +27,8 @@ def _case(R, K, D, dtype, learned, seed=0):
     ls = rng.normal(-1.2, 0.5, size=(R, K, D)).astype(np.float32) if learned else None
     s = np.exp(ls.astype(np.float64)) if learned else SIG_K[:K].astype(np.float64)[None, :, None]
     x = (mu64 + s * rng.normal(size=(R, K, D))).astype(np.float32)
-    x[3] = np.float32(np.nan) if R > 10 else x[3]   # a non-finite row: counted and masked
+    if R > 10:
+        x[3] = np.float32(np.nan)   # a non-finite row: counted and masked
     return mu, mu64, x, ls
 
 
@@ -39,7 +40,7 @@ def _err_scale(mu64, x, ls, K):
     return np.nan_to_num((0.5 * z * z + np.abs(lsig) + 1.0).sum(axis=(1, 2)), nan=1.0)
 
 
-SHAPES = [(300, 4, 70), (257, 4, 35), (50, 3, 200), (33, 1, 7)]
+SHAPES = [(300, 4, 70), (257, 4, 35), (50, 3, 200), (33, 1, 7), (3, 4, 70)]  # (3, ...): a lone partial tile
 
 
 @pytest.mark.parametrize("R,K,D", SHAPES)
@@ -69,7 +70,7 @@ def test_forward(R, K, D, dtype, learned):
 VARS = [dict(), dict(dual_clip=3.0, kl_coef=0.1), dict(ent_coef=0.01)]
 
 
-@pytest.mark.parametrize("R,K,D", SHAPES[:3])
+@pytest.mark.parametrize("R,K,D", SHAPES[:3] + SHAPES[4:])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("learned", [False, True])
 @pytest.mark.parametrize("var", VARS)
