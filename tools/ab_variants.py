@@ -12,7 +12,9 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
-    "nosmall": ("RLVLA_FLOW_SMALL_TILES=0",),
+    "noscan": ("RLVLA_SCATTER_SCAN_MAX=0",),
+    "stop1": ("RLVLA_SCATTER_STOP=1",),
+    "stop2": ("RLVLA_SCATTER_STOP=2",),
 }
 # name -> git revision whose csrc/ + include/ are built as one more variant
 # (the ABI only grew at the end of its structs, so today's binding drives older libraries)
