@@ -433,7 +433,7 @@ def run_ours(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, traj, logits, lb_fn=None,
-                                           n_env_sample=min(2, mb_envs))
+                                           n_env_sample=min(4, mb_envs))
     if rank == 0:
         print(json.dumps(out), flush=True)
     # the captured graph holds NCCL's persistent plans for the C1/C2/C3 collectives: release
