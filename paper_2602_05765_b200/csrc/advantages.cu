@@ -26,22 +26,36 @@ __device__ __forceinline__ bool step_ok_for_loss(int valid, int ver, const rlvla
 }
 
 // Tokens that will carry loss (target >= 0 on filled steps with 0 <= lag <= eta): one
-// warp per decision step over the whole grid; the step's key/version and its A token
-// loads are independent, so each iteration costs one memory round trip.
+// thread per token over the whole grid (the step's key/version are L1/L2 hits shared by
+// its A tokens), four independent tokens in flight per thread so each pass of the loop
+// costs one memory round trip whatever A is.
 __device__ __forceinline__ long long count_loss_tokens(const AdvArgs& a) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nsteps = int64_t(a.buf.n_env) * a.buf.t_steps;
-  const int A = a.buf.a_tok;
-  const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t A = a.buf.a_tok;
+  const int64_t ntok = int64_t(a.buf.n_env) * a.buf.t_steps * A;
+  const int64_t gt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nt = int64_t(gridDim.x) * blockDim.x;
   long long c = 0;
-  for (int64_t s = gw; s < nsteps; s += nw) {
-    const bool valid = a.buf.slot_key[s] != 0ull;
-    const int lag = a.p.cur_version - a.buf.version[s];
-    const int32_t* tk = a.buf.tokens + s * A;
-    int n = 0;
-    for (int j = lane; j < A; j += 32) n += tk[j] >= 0;
-    if (valid && lag >= 0 && lag <= a.p.max_staleness) c += n;
+  for (int64_t k0 = gt; k0 < ntok; k0 += 4 * nt) {
+    int tk[4], ver[4];
+    unsigned long long key[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t k = k0 + u * nt;
+      tk[u] = -1;
+      key[u] = 0ull;
+      ver[u] = 0;
+      if (k < ntok) {
+        const int64_t s = k / A;
+        tk[u] = a.buf.tokens[k];
+        key[u] = a.buf.slot_key[s];
+        ver[u] = a.buf.version[s];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int lag = a.p.cur_version - ver[u];
+      c += (key[u] != 0ull && lag >= 0 && lag <= a.p.max_staleness && tk[u] >= 0);
+    }
   }
   return c;
 }
@@ -295,12 +309,12 @@ int adv_grid(int E) {
   return g < 1 ? 1 : g;
 }
 
-// pass 1 also sweeps the E*T steps for the token count: ~2 steps per warp
-int pass1_grid(int E, int T) {
+// pass 1 also sweeps the E*T*A tokens for the token count: ~4 tokens per thread
+int pass1_grid(int E, int T, int A) {
   int g = adv_grid(E);
-  const int64_t steps = int64_t(E) * T;
-  int64_t gs = (steps + 2 * kWarpsPerBlock - 1) / (2 * kWarpsPerBlock);
-  const int cap = 2 * device_info().sm_count;
+  const int64_t toks = int64_t(E) * T * A;
+  int64_t gs = (toks + 4 * 256 - 1) / (4 * 256);
+  const int cap = 4 * device_info().sm_count;
   if (gs > cap) gs = cap;
   if (gs > g) g = int(gs);
   if (g > kMaxPartialBlocks) g = kMaxPartialBlocks;
@@ -310,7 +324,7 @@ int pass1_grid(int E, int T) {
 }  // namespace
 
 cudaError_t launch_adv_pass1(const AdvArgs& a, cudaStream_t s) {
-  const int g = pass1_grid(a.buf.n_env, a.buf.t_steps);
+  const int g = pass1_grid(a.buf.n_env, a.buf.t_steps, a.buf.a_tok);
   if (a.p.mode == RLVLA_ADV_GAE) gae_scan_kernel<<<g, 256, 0, s>>>(a);
   else grpo_returns_kernel<<<g, 256, 0, s>>>(a);
   return cudaGetLastError();

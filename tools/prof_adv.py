@@ -73,7 +73,7 @@ def main():
             med, mn = time_call(fn, args.iters)
             print(json.dumps({"shape": name, "mode": mode, "E_r": E, "T": T, "A": A,
                               "us_median": round(med, 2), "us_min": round(mn, 2),
-                              "ns_per_env_step": round(med * 1e3 / (E * T), 3)}), flush=True)
+                              "ns_per_slot": round(med * 1e3 / (E * T), 3)}), flush=True)
 
 
 if __name__ == "__main__":
