@@ -45,7 +45,7 @@ __device__ __forceinline__ long long count_loss_tokens(const AdvArgs& a) {
       key[u] = 0ull;
       ver[u] = 0;
       if (k < ntok) {
-        const int64_t s = k / A;
+        const int64_t s = ntok <= INT32_MAX ? int64_t(uint32_t(k) / uint32_t(A)) : k / A;
         tk[u] = a.buf.tokens[k];
         key[u] = a.buf.slot_key[s];
         ver[u] = a.buf.version[s];
@@ -314,7 +314,7 @@ int pass1_grid(int E, int T, int A) {
   int g = adv_grid(E);
   const int64_t toks = int64_t(E) * T * A;
   int64_t gs = (toks + 4 * 256 - 1) / (4 * 256);
-  const int cap = 4 * device_info().sm_count;
+  const int cap = 8 * device_info().sm_count;
   if (gs > cap) gs = cap;
   if (gs > g) g = int(gs);
   if (g > kMaxPartialBlocks) g = kMaxPartialBlocks;
