@@ -145,3 +145,25 @@ def test_advantages_deterministic():
         outs.append((adv, ret, st))
     for o in outs[1:]:
         assert all(torch.equal(a, b) for a, b in zip(o, outs[0]))
+
+
+def test_gae_token_count_multipass():
+    """Loss-token count when the token sweep needs several grid passes and ends ragged:
+    512 x 300 x 9 = 1,382,400 tokens > 8 CTAs/SM x 256 threads x 4 tokens per pass,
+    negative targets and stale/bad versions mixed in (oracle step_counts)."""
+    P = _P()
+    reward, value, done, valid, ver, _, lv = _gae_case(300, 512, 11, 0.01, 0.95)
+    rng = np.random.default_rng(12)
+    tokens = rng.integers(-2, 40, size=(512, 300, 9)).astype(np.int32)
+    ver = (100 - rng.integers(-1, 4, size=(512, 300))).astype(np.int32)
+    buf = _gpu_buffer(reward, value, done, valid, ver, tokens)
+    adv = torch.zeros(512, 300, device="cuda")
+    ret = torch.zeros(512, 300, device="cuda")
+    stats = torch.zeros(24, dtype=torch.float64, device="cuda")
+    prm = P.adv_params("gae", n_env_global=512, cur_version=100, max_staleness=1)
+    P.rlvla_advantages(buf, torch.from_numpy(lv).cuda(), prm, adv, ret, stats, P.workspace(512))
+    st = stats.cpu().numpy()
+    c = O_adv.step_counts(valid, ver, tokens, 100, 1)
+    assert (st[3], st[4], st[5]) == (c["n_tok"], c["n_stale"], c["n_bad"])
+    a, _ = O_adv.gae(reward, value, done, valid, lv, 0.99, 0.95)
+    H.assert_close_rel(adv.cpu().numpy(), a, 1e-5, max(1e-3, float(np.sqrt(np.mean(a ** 2)))), "adv")
