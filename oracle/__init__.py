@@ -29,7 +29,12 @@ Functions and their pins (tests/test_oracle_*.py, all `-m "not gpu"`):
   advantages.grpo            S2b Shao et al. 2024 (GRPO); reading R10.
       pins: printed values for {0,1} and {1,0,0,0} groups (unbiased and population),
             zero-sum, affine invariance, all-equal => 0, singleton => 0.
-  advantages.step_counts     token/stale counts; pins: brute-force loop on tiny inputs.
+  advantages.episode_return, advantages.grpo_step_adv, advantages.step_counts
+                             S2b / pre-loss glue. pins (tests/test_oracle_path.py): a
+            hand-built 2-groups-of-4 buffer whose unfilled slots hold junk rewards and stale
+            versions, answered by the printed GRPO values and a closed form (SURVEY §8(c)
+            S2b (vi)); per-element broadcast table; closed-form counts with stale, future,
+            ignored and unfilled steps (plus the brute-force loop in test_oracle_advantages).
   logprob.log_softmax_gather S3  P:39 (§2, action tokens); readings R3, R4, R5.
       pins: sum_j exp(logp_j) = 1, uniform row = -ln V, saturation,
             shift invariance, tied maxima, -inf columns, entropy closed forms.
@@ -40,7 +45,16 @@ Functions and their pins (tests/test_oracle_*.py, all `-m "not gpu"`):
       pins: clip table, ratio == 1, decoupled(prox = behav) ==
             standard, staleness lag = eta / eta+1 / -1, finite differences of the
             composed loss, micro-batch split invariance.
-  path.rollout_to_loss       S1..S4 composed; pins follow from the above plus the
+  path.advantages            S2 on a buffer (valid = slot_key != 0). pins: the GRPO
+            brute force above; GAE gamma = lambda = 1 segment counts with a junk-filled unfilled
+            slot and whitening against numpy std (ddof = 1); P = 1 vs P = 2, 8 logical shards
+            (GRPO bit-identical, whitened GAE within 1e-12: SURVEY §8(c) S2b (vii), S2a (vii)).
+  path.token_view            row r <-> token r % A of step r // A, lag = cur - version:
+            a hand-built 2 x 3 x 2 buffer with every expected row written out.
+  path.loss_and_grad         S3 + S4 composed. pins: torch fp64 autograd of the composed
+            objective (tests/test_oracle_next2.py), the clip table and finite differences.
+  path.rollout_to_loss       S1..S4 composed. pins: a hand-evaluable 2-env GRPO case
+            (counters, A = +-0.707105781, Loss = -A/3, g and dx in closed form) plus the
             Eq. (2) throughput unit (tests/golden/eq2_throughput.csv).
 
 No function here is "parity unpinned".
