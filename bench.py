@@ -404,7 +404,11 @@ def run_ours(args):
                    "groups_span_ranks": bool(groups_span),
                    "l2": f"inputs larger than L2: {R * V * 2 / 1e9:.1f} GB logits read + same "
                          "written per step per GPU, no flush needed",
-                   "parallelism": f"dp{world}"},
+                   "parallelism": f"dp{world}",
+                   "nranks": world,
+                   "collectives": ("none (1 rank)" if comm is None else
+                                   "C1/C2/C3 in-kernel over NVLink peer memory (CUDA IPC mailboxes)"
+                                   if comm.p2p else "C1/C2/C3 NCCL collectives on the step stream")},
         "clocks": clocks,
         "e2e": None if e2e_ms is None else {
             "value": units_per_step * args.steps / (e2e_ms / 1e3), "unit": UNIT,

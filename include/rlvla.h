@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define RLVLA_ABI_VERSION 1
+#define RLVLA_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define RLVLA_API __attribute__((visibility("default")))
@@ -67,7 +67,7 @@ enum {
 typedef enum { RLVLA_F32 = 0, RLVLA_BF16 = 1 } rlvla_dtype;
 
 /* Statistics vector: double[RLVLA_NSTATS], device memory, slots below.
- * rlvla_advantages writes slots 0..5 (and allreduces them over `comm`);
+ * rlvla_advantages writes slots 0..5 and 23 (and allreduces them over `comm`);
  * rlvla_logprob_fwd_bwd / rlvla_ppo_loss write slots 6..18 (allreducing 6..17);
  * rlvla_value_loss writes slots 19..22 (allreducing 19..21).
  * Each call OVERWRITES its slots unless `accumulate` is set (Streamer micro-batches). */
@@ -96,7 +96,8 @@ enum {
   RLVLA_STAT_N_VALUE_CLIPPED = 20, /* #steps on the clipped value branch                */
   RLVLA_STAT_N_VALUE_STEPS = 21,   /* sum_s m_s                                         */
   RLVLA_STAT_VALUE_DENOM = 22,     /* the N_v used                                      */
-  RLVLA_STAT_RESERVED = 23,
+  RLVLA_STAT_N_LOSS_STEPS = 23,    /* #filled steps with 0<=lag<=eta and >= 1 target>=0: */
+                                   /* the chunk-ratio normaliser N_steps (R21), global  */
   RLVLA_NSTATS = 24
 };
 
@@ -189,7 +190,7 @@ typedef struct {
  * delta_t = v_t (r_t + gamma (nt_t V_{t+1} + tr_t B_t) - V_t) with V_T = last_value[e]
  * (NULL => 0), B = boot_value; A_t = delta_t + gamma lam nt_t A_{t+1}. Computed as a warp-parallel suffix scan of the
  * affine maps A -> delta_t + c_t A (fp32, fp64 statistics).
- * stats: device double[RLVLA_NSTATS]; slots 0..5 written and reduced over `comm` (C1). With
+ * stats: device double[RLVLA_NSTATS]; slots 0..5 and 23 written and reduced over `comm` (C1). With
  * GRPO and comm != NULL the per-env returns are allgathered (C2) first. */
 RLVLA_API rlvla_status rlvla_advantages(const rlvla_traj_buffer* buf, const float* last_value,
                               const rlvla_adv_params* p, float* adv, float* ret,
@@ -242,7 +243,14 @@ typedef struct {
                               /* the logits (logits path only; 0 in rlvla_ppo_loss)     */
   int32_t ratio_level;        /* rlvla_ppo_loss only: 0 token ratio; 1 one ratio per     */
                               /* decision step = the action chunk's likelihood ratio    */
-                              /* exp(sum_a m (logp - logp_behav)), Loss / N_steps       */
+                              /* exp(sum_a m (logp - logp_behav)) (decoupled: w_s =     */
+                              /* min(exp(sum m (logp_prox - logp_behav)), is_cap),      */
+                              /* rho_s = exp(sum m (logp - logp_prox)); dual_clip as    */
+                              /* above; kl_coef / ent_coef => RLVLA_ERR_UNSUPPORTED),    */
+                              /* Loss / N_steps with N_steps = tok_denominator (> 0),   */
+                              /* else adv_stats[RLVLA_STAT_N_LOSS_STEPS] (global), else  */
+                              /* the call's own masked-step count over all ranks of     */
+                              /* `comm` (not allowed with accumulate = 1)               */
 } rlvla_ppo_args;
 
 /* S3 (+S4) — action-token log-probs over logit rows (P:39 action tokens; P:88 actor
@@ -281,8 +289,8 @@ RLVLA_API rlvla_status rlvla_ppo_loss(const float* logp, int64_t rows, const int
 /* S4 value head (reading R22): clipped value loss per decision step,
  *   L_s = 0.5 max((v - R)^2, (v_old + clip(v - v_old, -clip_eps, clip_eps) - R)^2)
  * (clip_eps <= 0 => 0.5 (v - R)^2), m_s = [slot_key != 0][0 <= lag <= max_staleness],
- * Loss = sum m L / N_v with N_v = denominator (> 0) or the call's sum m_s (then per rank;
- * pass an explicit global N_v with comm). grad_v[s] = dLoss/dv_s (required), loss_step
+ * Loss = sum m L / N_v with N_v = denominator (> 0) or the call's sum m_s over all ranks of
+ * `comm` (the gradient scale waits for the reduced count). grad_v[s] = dLoss/dv_s (required), loss_step
  * optional. v_new, v_old (= buffer value), ret: float[n_steps]. stats slots 19..22 (C over
  * comm for 19..21). */
 RLVLA_API rlvla_status rlvla_value_loss(const float* v_new, const float* v_old, const float* ret,
@@ -402,11 +410,29 @@ RLVLA_API rlvla_status rlvla_flow_logprob(const rlvla_gauss_chain* c, float* log
 RLVLA_API size_t rlvla_workspace_bytes(int64_t rows, int32_t n_env_global, int32_t t_steps);
 
 /* Communicator over NCCL (NVLink/NVSwitch). Rank 0 calls rlvla_comm_unique_id and the
- * 128 bytes are broadcast by the caller (e.g. torch.distributed). Host pointers. */
+ * 128 bytes are broadcast by the caller (e.g. torch.distributed). Host pointers. Every
+ * rank takes part in the same collectives at init whatever its local result (a rank whose
+ * mailbox could not be mapped makes all ranks fall back to NCCL collectives together). */
 RLVLA_API rlvla_status rlvla_comm_unique_id(void* out_id_128_bytes);
 RLVLA_API rlvla_status rlvla_comm_init(const void* nccl_unique_id, int32_t nranks, int32_t rank,
                              rlvla_comm* out);
 RLVLA_API rlvla_status rlvla_comm_destroy(rlvla_comm c);
+
+/* P2P-only communicator (no NCCL): the cross-rank exchanges C1/C2/C3 run only inside the
+ * kernels over CUDA-IPC-mapped mailboxes, so several ranks may share one GPU (NCCL refuses
+ * duplicate devices) and up to 8 ranks are supported. Two phases, the handle exchange done
+ * by the caller over its own process group (e.g. a torch gloo all_gather):
+ *   1. rlvla_comm_init_p2p: allocates this rank's mailbox on the current device and writes
+ *      its IPC handle (RLVLA_P2P_HANDLE_BYTES host bytes) to out_handle;
+ *   2. rlvla_comm_connect_p2p: all_handles = host [nranks][RLVLA_P2P_HANDLE_BYTES] in rank
+ *      order; maps every peer's mailbox. A failure returns RLVLA_ERR_CUDA; the caller must
+ *      agree on the outcome across ranks and destroy the communicator on any failure.
+ * Calls that would need an NCCL collective with such a communicator (GRPO with
+ * n_env_global > 32768) return RLVLA_ERR_UNSUPPORTED. */
+#define RLVLA_P2P_HANDLE_BYTES 64
+RLVLA_API rlvla_status rlvla_comm_init_p2p(int32_t nranks, int32_t rank, void* out_handle,
+                                           rlvla_comm* out);
+RLVLA_API rlvla_status rlvla_comm_connect_p2p(rlvla_comm c, const void* all_handles);
 /* 1 when the communicator reduces statistics INSIDE the computing kernel over NVLink peer
  * memory (every rank's mailbox mapped through CUDA IPC at rlvla_comm_init; the kernel's last
  * CTA pushes its slots to all ranks and sums them in rank order): C1 and the GRPO returns

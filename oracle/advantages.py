@@ -113,6 +113,8 @@ def step_counts(valid, version, tokens, cur_version: int, max_staleness: int):
          n_tok    = #tokens with target >= 0 on valid steps with 0 <= lag <= eta
          n_stale  = #valid steps with lag > eta
          n_bad    = #valid steps with lag < 0
+         n_loss_steps = #valid steps with 0 <= lag <= eta and >= 1 token with target >= 0
+                    (the chunk-ratio normaliser N_steps, reading R21)
     lag = cur_version - version (rollout runs on pre-update weights => lag <= 1)."""
     v = np.asarray(valid, bool)
     lag = cur_version - np.asarray(version, np.int64)
@@ -120,4 +122,5 @@ def step_counts(valid, version, tokens, cur_version: int, max_staleness: int):
     tok_ok = (np.asarray(tokens) >= 0).sum(axis=2)
     return dict(n_valid=int(v.sum()), n_tok=int((tok_ok * ok).sum()),
                 n_stale=int((v & (lag > max_staleness)).sum()),
-                n_bad=int((v & (lag < 0)).sum()))
+                n_bad=int((v & (lag < 0)).sum()),
+                n_loss_steps=int((ok & (tok_ok > 0)).sum()))

@@ -101,35 +101,57 @@ def ppo_loss(logp, logp_behav, adv_tok, mask_base, lag_tok, *, eps_low=0.2, eps_
 
 
 def ppo_loss_chunk(logp, logp_behav, adv_step, mask_tok, step_of_tok, n_steps_total, *,
-                   eps_low=0.2, eps_high=0.2, n_den=None):
+                   eps_low=0.2, eps_high=0.2, n_den=None, logp_prox=None, is_cap=0.0,
+                   dual_clip=0.0):
     """Chunk-level ratio (NEXT-2, reading R21): one ratio per decision step = the action
     chunk's likelihood ratio rho_s = exp(sum_{a in s, m_a} (logp_a - logp_behav_a)) (an
     OpenVLA-OFT action chunk is one inference); L_s = -min(rho_s A_s, clip(rho_s) A_s)
     over steps with >= 1 masked token; Loss = sum_s L_s / N_steps; every token of step s gets
-    dLoss/dlogp = -A_s rho_s [active_s] / N_steps."""
+    dLoss/dlogp = -A_s rho_s [active_s] / N_steps.
+    Decoupled (R12 at step level): w_s = min(exp(sum m (logp_prox - logp_behav)), cap)
+    (detached), rho_s = exp(sum m (logp - logp_prox)), L_s = -w_s J_s. Dual clip (R19 at step
+    level): for A_s < 0, J_s = max(J_s, c A_s); steps with c A_s > J_s carry no gradient."""
     logp = np.asarray(logp, np.float64)
     lb = np.asarray(logp_behav, np.float64)
     m = np.asarray(mask_tok, bool)
     st = np.asarray(step_of_tok, np.int64)
     A = np.asarray(adv_step, np.float64)
+    lpp = None if logp_prox is None else np.asarray(logp_prox, np.float64)
     lr = np.zeros(n_steps_total)
+    lw = np.zeros(n_steps_total)
     cnt = np.zeros(n_steps_total)
     for r in range(len(logp)):
         if m[r]:
-            lr[st[r]] += logp[r] - lb[r]
+            if lpp is None:
+                lr[st[r]] += logp[r] - lb[r]
+            else:
+                lr[st[r]] += logp[r] - lpp[r]
+                lw[st[r]] += lpp[r] - lb[r]
             cnt[st[r]] += 1
     ms = cnt > 0
     N = float(ms.sum()) if n_den is None else n_den
     inv = 1.0 / N if N > 0 else 0.0
     rho = np.exp(lr)
+    w = np.ones(n_steps_total) if lpp is None else np.exp(lw)
+    if lpp is not None and is_cap and is_cap > 0:
+        w = np.minimum(w, is_cap)
     lo, hi = 1.0 - eps_low, 1.0 + eps_high
     J = np.minimum(rho * A, np.clip(rho, lo, hi) * A)
     clipped = ((A > 0) & (rho > hi)) | ((A < 0) & (rho < lo))
-    g_step = np.where(ms & ~clipped, -A * rho * inv, 0.0)
+    dual = np.zeros(n_steps_total, bool)
+    if dual_clip and dual_clip > 1.0:
+        dual = (A < 0) & (dual_clip * A > J)
+        J = np.where(dual, dual_clip * A, J)
+    g_step = np.where(ms & ~clipped & ~dual, -w * A * rho * inv, 0.0)
     grad = np.where(m, g_step[st], 0.0)
-    L = np.where(ms, -J, 0.0)
-    return dict(grad=grad, loss_step=L, rho_step=rho, mask_step=ms, clipped=clipped & ms,
+    L = np.where(ms, -w * J, 0.0)
+    near = (np.abs(rho / hi - 1.0) <= NEAR_TIE_REL) | (np.abs(rho / lo - 1.0) <= NEAR_TIE_REL)
+    if dual_clip and dual_clip > 1.0:
+        near = near | (np.abs(rho / dual_clip - 1.0) <= NEAR_TIE_REL)
+    return dict(grad=grad, loss_step=L, rho_step=rho, w_step=w, mask_step=ms,
+                clipped=clipped & ms, dual=dual & ms, near_tie_step=near & ms,
                 stats=dict(loss=L.sum() * inv, n_clipped=float((clipped & ms).sum()),
+                           n_dual_clipped=float((dual & ms).sum()),
                            n_steps=float(ms.sum()), denom=N))
 
 

@@ -21,8 +21,9 @@ NSTATS = 24
  STAT_N_BAD_STEPS, STAT_LOSS, STAT_N_CLIPPED, STAT_KL_K3_SUM, STAT_ENTROPY_SUM,
  STAT_RATIO_SUM, STAT_N_LOSS_TOK, STAT_N_STALE_TOK, STAT_N_BAD_TOK, STAT_LOGP_SUM,
  STAT_KL_REF_SUM, STAT_N_DUAL_CLIPPED, STAT_PG_LOSS, STAT_DENOM, STAT_VALUE_LOSS,
- STAT_N_VALUE_CLIPPED, STAT_N_VALUE_STEPS, STAT_VALUE_DENOM, STAT_RESERVED) = range(24)
+ STAT_N_VALUE_CLIPPED, STAT_N_VALUE_STEPS, STAT_VALUE_DENOM, STAT_N_LOSS_STEPS) = range(24)
 CNT_OOB, CNT_BAD_VERSION, CNT_DUP, CNT_WRITTEN = range(4)
+P2P_HANDLE_BYTES = 64           # RLVLA_P2P_HANDLE_BYTES (cudaIpcMemHandle_t)
 
 
 class c_traj_buffer(ctypes.Structure):
@@ -102,6 +103,8 @@ _SIGS = {
     "rlvla_comm_init": (c_int32, [c_void_p, c_int32, c_int32, POINTER(c_void_p)]),
     "rlvla_comm_destroy": (c_int32, [c_void_p]),
     "rlvla_comm_p2p_enabled": (c_int32, [c_void_p]),
+    "rlvla_comm_init_p2p": (c_int32, [c_int32, c_int32, c_void_p, POINTER(c_void_p)]),
+    "rlvla_comm_connect_p2p": (c_int32, [c_void_p, c_void_p]),
     "rlvla_status_string": (ctypes.c_char_p, [c_int32]),
     "rlvla_abi_version": (c_int32, []),
     "rlvla_nccl_version": (c_int32, []),

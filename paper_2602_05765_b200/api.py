@@ -309,26 +309,59 @@ def rlvla_nccl_version() -> int:
 
 
 class Comm:
-    """rlvla_comm over NCCL; the 128-byte unique id travels over a torch ProcessGroup."""
+    """rlvla_comm: over NCCL (from_process_group; the 128-byte unique id travels over a torch
+    ProcessGroup) or P2P-only (p2p_from_process_group; CUDA IPC mailbox handles travel over
+    the ProcessGroup, no NCCL: several ranks may share a GPU)."""
 
     def __init__(self, handle, nranks, rank):
         self.handle, self.nranks, self.rank = handle, nranks, rank
 
+    @staticmethod
+    def _group_info(group):
+        import torch.distributed as dist
+        return dist.get_rank(group), dist.get_world_size(group), dist.get_backend(group)
+
     @classmethod
     def from_process_group(cls, group=None, device=None):
         import torch.distributed as dist
-        rank, n = dist.get_rank(group), dist.get_world_size(group)
+        rank, n, backend = cls._group_info(group)
         uid = (ctypes.c_ubyte * 128)()
         if rank == 0:
             _check(lib().rlvla_comm_unique_id(uid), "rlvla_comm_unique_id", True)
-        backend = dist.get_backend(group)
         dev = device if (backend == "nccl") else "cpu"
         t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device=dev)
-        dist.broadcast(t, src=0, group=group)
+        # group_src: the GROUP's rank 0 (src would be a global rank)
+        dist.broadcast(t, group_src=0, group=group)
         raw = bytes(t.cpu().tolist())
         uid2 = (ctypes.c_ubyte * 128).from_buffer_copy(raw)
         h = ctypes.c_void_p()
         _check(lib().rlvla_comm_init(uid2, n, rank, ctypes.byref(h)), "rlvla_comm_init", True)
+        return cls(h, n, rank)
+
+    @classmethod
+    def p2p_from_process_group(cls, group=None):
+        """P2P-only communicator on the current CUDA device: every rank allocates its mailbox,
+        the IPC handles are allgathered over `group` (any backend, e.g. gloo), every rank maps
+        its peers, and the outcome is agreed over `group` (any failure raises everywhere)."""
+        import torch.distributed as dist
+        rank, n, _ = cls._group_info(group)
+        hb = A.P2P_HANDLE_BYTES
+        mine = (ctypes.c_ubyte * hb)()
+        h = ctypes.c_void_p()
+        st = lib().rlvla_comm_init_p2p(n, rank, mine, ctypes.byref(h))
+        recs = [None] * n
+        dist.all_gather_object(recs, (int(st), bytes(mine)), group=group)
+        ok = all(r[0] == A.OK for r in recs)
+        if ok:
+            allh = (ctypes.c_ubyte * (hb * n)).from_buffer_copy(b"".join(r[1] for r in recs))
+            ok = lib().rlvla_comm_connect_p2p(h, allh) == A.OK
+        votes = [None] * n
+        dist.all_gather_object(votes, bool(ok), group=group)
+        if not all(votes):
+            if h:
+                lib().rlvla_comm_destroy(h)
+            raise RlvlaError(A.ERR_CUDA if st == A.OK else st,
+                             f"rlvla_comm_init_p2p/connect (ranks ok: {votes})")
         return cls(h, n, rank)
 
     @property

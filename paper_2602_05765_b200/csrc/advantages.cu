@@ -28,15 +28,22 @@ __device__ __forceinline__ bool step_ok_for_loss(int valid, int ver, const rlvla
 // Tokens that will carry loss (target >= 0 on filled steps with 0 <= lag <= eta): one
 // thread per token over the whole grid (the step's key/version are L1/L2 hits shared by
 // its A tokens), four independent tokens in flight per thread so each pass of the loop
-// costs one memory round trip whatever A is.
-__device__ __forceinline__ long long count_loss_tokens(const AdvArgs& a) {
+// costs one memory round trip whatever A is. The thread holding a step's token 0 also
+// counts the step as a loss step (the chunk-ratio normaliser, slot N_LOSS_STEPS) when
+// one of its tokens has target >= 0: its own token decides unless it is ignored (-1),
+// only then are the step's later tokens read.
+struct LossCounts {
+  long long tok, steps;
+};
+__device__ __forceinline__ LossCounts count_loss_tokens(const AdvArgs& a) {
   const int64_t A = a.buf.a_tok;
   const int64_t ntok = int64_t(a.buf.n_env) * a.buf.t_steps * A;
   const int64_t gt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nt = int64_t(gridDim.x) * blockDim.x;
-  long long c = 0;
+  LossCounts c{0, 0};
   for (int64_t k0 = gt; k0 < ntok; k0 += 4 * nt) {
     int tk[4], ver[4];
+    bool first[4];
     unsigned long long key[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -44,17 +51,26 @@ __device__ __forceinline__ long long count_loss_tokens(const AdvArgs& a) {
       tk[u] = -1;
       key[u] = 0ull;
       ver[u] = 0;
+      first[u] = false;
       if (k < ntok) {
         const int64_t s = ntok <= INT32_MAX ? int64_t(uint32_t(k) / uint32_t(A)) : k / A;
         tk[u] = a.buf.tokens[k];
         key[u] = a.buf.slot_key[s];
         ver[u] = a.buf.version[s];
+        first[u] = k == s * A;
       }
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int lag = a.p.cur_version - ver[u];
-      c += (key[u] != 0ull && lag >= 0 && lag <= a.p.max_staleness && tk[u] >= 0);
+      const bool ok = key[u] != 0ull && lag >= 0 && lag <= a.p.max_staleness;
+      c.tok += (ok && tk[u] >= 0);
+      if (ok && first[u]) {
+        bool has = tk[u] >= 0;
+        const int64_t k = k0 + u * nt;
+        for (int64_t j = 1; !has && j < A; ++j) has = a.buf.tokens[k + j] >= 0;
+        c.steps += has;
+      }
     }
   }
   return c;
@@ -136,15 +152,17 @@ __global__ void __launch_bounds__(256) gae_scan_kernel(AdvArgs a) {
       carry_v = __shfl_sync(0xffffffffu, v, 0);
     }
   }
-  s_tok += count_loss_tokens(a);
-  // CTA partials: warp reduce then fixed-order over warps
-  __shared__ double red[kWarpsPerBlock][6];
+  const LossCounts lc = count_loss_tokens(a);
+  s_tok += lc.tok;
+  // CTA partials: warp reduce then fixed-order over warps (slot 6 -> stats[N_LOSS_STEPS])
+  __shared__ double red[kWarpsPerBlock][7];
   s_n = warp_sum_d(s_n);
   s_a = warp_sum_d(s_a);
   s_a2 = warp_sum_d(s_a2);
   const double t_tok = double(warp_sum_ll(s_tok));
   const double t_st = double(warp_sum_ll(s_stale));
   const double t_bad = double(warp_sum_ll(s_bad));
+  const double t_steps = double(warp_sum_ll(lc.steps));
   if (lane == 0) {
     red[warp][0] = s_n;
     red[warp][1] = s_a;
@@ -152,17 +170,19 @@ __global__ void __launch_bounds__(256) gae_scan_kernel(AdvArgs a) {
     red[warp][3] = t_tok;
     red[warp][4] = t_st;
     red[warp][5] = t_bad;
+    red[warp][6] = t_steps;
   }
   __syncthreads();
-  if (threadIdx.x < 6) {
+  if (threadIdx.x < 7) {
     double acc = 0;
     for (int w = 0; w < kWarpsPerBlock; ++w) acc += red[w][threadIdx.x];
     a.ws.partials[size_t(blockIdx.x) * RLVLA_NSTATS + threadIdx.x] = acc;
   }
-  __shared__ double tot[6];
-  if (last_block_reduce(a.ws.ctrl + CTRL_ADV, a.ws.partials, 6, tot)) {
-    if (a.ws.p2p.nranks > 1) p2p_exchange(tot, 6, a.ws.p2p);  // C1 in-kernel (NVLink)
+  __shared__ double tot[7];
+  if (last_block_reduce(a.ws.ctrl + CTRL_ADV, a.ws.partials, 7, tot)) {
+    if (a.ws.p2p.nranks > 1) p2p_exchange(tot, 7, a.ws.p2p);  // C1 in-kernel (NVLink)
     if (threadIdx.x < 6) a.stats[threadIdx.x] = tot[threadIdx.x];
+    if (threadIdx.x == 6) a.stats[RLVLA_STAT_N_LOSS_STEPS] = tot[6];
   }
 }
 
@@ -199,34 +219,39 @@ __global__ void __launch_bounds__(256) grpo_returns_kernel(AdvArgs a) {
     R = warp_sum(R);  // fixed xor tree: identical for any rank count
     if (lane == 0) a.ws.r_global[a.p.env_offset + e] = R;
   }
-  s_tok += count_loss_tokens(a);
-  __shared__ double red[kWarpsPerBlock][4];
+  const LossCounts lc = count_loss_tokens(a);
+  s_tok += lc.tok;
+  __shared__ double red[kWarpsPerBlock][5];
   s_n = warp_sum_d(s_n);
   const double t_tok = double(warp_sum_ll(s_tok));
   const double t_st = double(warp_sum_ll(s_stale));
   const double t_bad = double(warp_sum_ll(s_bad));
+  const double t_steps = double(warp_sum_ll(lc.steps));
   if (lane == 0) {
     red[warp][0] = s_n;
     red[warp][1] = t_tok;
     red[warp][2] = t_st;
     red[warp][3] = t_bad;
+    red[warp][4] = t_steps;
   }
   __syncthreads();
-  if (threadIdx.x < 6) {
+  if (threadIdx.x < 7) {
     double acc = 0;
     const int tx = int(threadIdx.x);
-    const int src = tx == 0 ? 0 : (tx >= 3 ? tx - 2 : -1);  // slots 0,3,4,5 <- red 0..3
+    // slots 0,3,4,5,6 <- red 0..4 (slot 6 -> stats[N_LOSS_STEPS]); slots 1,2 = 0
+    const int src = tx == 0 ? 0 : (tx >= 3 ? tx - 2 : -1);
     if (src >= 0)
       for (int w = 0; w < kWarpsPerBlock; ++w) acc += red[w][src];
-    a.ws.partials[size_t(blockIdx.x) * RLVLA_NSTATS + threadIdx.x] = acc;  // slots 1,2 = 0
+    a.ws.partials[size_t(blockIdx.x) * RLVLA_NSTATS + threadIdx.x] = acc;
   }
-  __shared__ double tot[6];
-  if (last_block_reduce(a.ws.ctrl + CTRL_ADV, a.ws.partials, 6, tot)) {
+  __shared__ double tot[7];
+  if (last_block_reduce(a.ws.ctrl + CTRL_ADV, a.ws.partials, 7, tot)) {
     // C1 + C2 in-kernel (NVLink): statistics summed, every rank's returns gathered
     if (a.ws.p2p.nranks > 1)
-      p2p_exchange(tot, 6, a.ws.p2p, a.ws.r_global + a.p.env_offset, a.p.env_offset, E, a.ws.r_global,
+      p2p_exchange(tot, 7, a.ws.p2p, a.ws.r_global + a.p.env_offset, a.p.env_offset, E, a.ws.r_global,
                    a.p.n_env_global);
     if (threadIdx.x < 6) a.stats[threadIdx.x] = tot[threadIdx.x];
+    if (threadIdx.x == 6) a.stats[RLVLA_STAT_N_LOSS_STEPS] = tot[6];
   }
 }
 

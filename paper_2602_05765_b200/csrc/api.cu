@@ -24,7 +24,7 @@ struct NvtxRange {
 }  // namespace
 
 struct rlvla_comm_s {
-  ncclComm_t comm;
+  ncclComm_t comm = nullptr;  // NULL for a P2P-only communicator (rlvla_comm_init_p2p)
   int nranks;
   int rank;
   // in-kernel NVLink reduction (P2PDesc): own mailbox, peers' mailboxes mapped by CUDA IPC
@@ -98,8 +98,9 @@ rlvla_status check_buffer(const rlvla_traj_buffer* b) {
   return RLVLA_OK;
 }
 
-rlvla_status check_ppo_args(const rlvla_ppo_args* f) {
-  if (!f->logp_behav || !f->adv || !f->version || !f->slot_key) return RLVLA_ERR_INVALID_ARG;
+// rows == 0 (a rank or micro-batch without rows) allows NULL per-row / per-step arrays
+rlvla_status check_ppo_args(const rlvla_ppo_args* f, int64_t rows) {
+  if (rows > 0 && (!f->logp_behav || !f->adv || !f->version || !f->slot_key)) return RLVLA_ERR_INVALID_ARG;
   if (f->a_tok <= 0 || f->max_staleness < 0) return RLVLA_ERR_INVALID_ARG;
   if (!(f->eps_low >= 0.f) || !(f->eps_high >= 0.f) || f->eps_low >= 1.f) return RLVLA_ERR_INVALID_ARG;
   if (!(f->tok_denominator > 0.0) && !f->adv_stats && f->ratio_level == 0) return RLVLA_ERR_INVALID_ARG;
@@ -107,10 +108,16 @@ rlvla_status check_ppo_args(const rlvla_ppo_args* f) {
   if (f->accumulate != 0 && f->accumulate != 1) return RLVLA_ERR_INVALID_ARG;
   if (f->ratio_level != 0 && f->ratio_level != 1) return RLVLA_ERR_INVALID_ARG;
   if (!(f->dual_clip <= 0.f || f->dual_clip > 1.f)) return RLVLA_ERR_INVALID_ARG;
-  if (f->kl_coef != 0.f && !f->logp_ref) return RLVLA_ERR_INVALID_ARG;
+  if (f->kl_coef != 0.f && !f->logp_ref && rows > 0) return RLVLA_ERR_INVALID_ARG;
   if (!(f->ent_coef == f->ent_coef) || !(f->kl_coef == f->kl_coef)) return RLVLA_ERR_INVALID_ARG;
+  // chunk ratio with the call's own step count: micro-batches would each normalise by their
+  // own count, so accumulate needs N_steps up front (explicit or from rlvla_advantages)
+  if (f->ratio_level == 1 && !(f->tok_denominator > 0.0) && !f->adv_stats && f->accumulate)
+    return RLVLA_ERR_INVALID_ARG;
   return RLVLA_OK;
 }
+
+bool multi_rank(rlvla_comm c) { return c && c->nranks > 1; }
 
 // the in-kernel reduction descriptor for a call that reduces its loss statistics over `c`
 P2PDesc p2p_desc(rlvla_comm c, int ch) {
@@ -127,6 +134,7 @@ bool uses_p2p(rlvla_comm c) { return c && c->p2p && c->nranks > 1; }
 
 rlvla_status allreduce_stats(double* p, int n, rlvla_comm c, cudaStream_t s) {
   if (!c || c->nranks <= 1) return RLVLA_OK;
+  if (!c->comm) return RLVLA_ERR_UNSUPPORTED;  // P2P-only communicator: no NCCL fallback
   return ncclAllReduce(p, p, size_t(n), ncclDouble, ncclSum, c->comm, s) == ncclSuccess
              ? RLVLA_OK
              : RLVLA_ERR_NCCL;
@@ -139,6 +147,24 @@ rlvla_status sync_check_stats(const double* stats, int slot, cudaStream_t s) {
       cudaStreamSynchronize(s) != cudaSuccess)
     return RLVLA_ERR_CUDA;
   return v != 0.0 ? RLVLA_ERR_DATA : RLVLA_OK;
+}
+
+// Loss statistics of a call with no rows on this rank (logits / flow paths): one CTA of the
+// token-level S4 kernel over zero rows writes the call's totals (zeros, or the running
+// totals with accumulate) and joins C3 on the same channel as the computing kernels.
+rlvla_status stats_only_call(const rlvla_ppo_args& f, double* stats, void* workspace,
+                             rlvla_comm comm, cudaStream_t s) {
+  PpoArgs a{};
+  a.rows = 0;
+  a.f = f;
+  a.f.ratio_level = 0;
+  a.stats = stats;
+  a.ws = carve(workspace);
+  const bool p2p = uses_p2p(comm);
+  if (p2p) a.ws.p2p = p2p_desc(comm, P2P_CH_LOSS);
+  rlvla_status st = cuda_status(launch_ppo_loss(a, s));
+  if (st != RLVLA_OK || p2p) return st;
+  return allreduce_stats(stats + RLVLA_STAT_LOSS, RLVLA_STAT_DENOM - RLVLA_STAT_LOSS, comm, s);
 }
 
 }  // namespace
@@ -222,12 +248,16 @@ RLVLA_API rlvla_status rlvla_advantages(const rlvla_traj_buffer* buf, const floa
   AdvArgs a{*buf, last_value, *p, adv, ret, stats, carve(workspace)};
   // C1 (+ C2) inside the pass-1 kernel over NVLink when the mailbox can hold the returns
   const bool p2p = uses_p2p(comm) && p->n_env_global <= kP2PMaxEnvGlobal;
+  if (!p2p && multi_rank(comm) && !comm->comm) return RLVLA_ERR_UNSUPPORTED;
   if (p2p) a.ws.p2p = p2p_desc(comm, P2P_CH_ADV);
   st = cuda_status(launch_adv_pass1(a, s));
   if (st != RLVLA_OK) return st;
   if (!p2p && comm && comm->nranks > 1) {
+    if (!comm->comm) return RLVLA_ERR_UNSUPPORTED;  // P2P-only communicator, mailbox too small
     if (ncclGroupStart() != ncclSuccess) return RLVLA_ERR_NCCL;
     ncclResult_t r1 = ncclAllReduce(stats, stats, 6, ncclDouble, ncclSum, comm->comm, s);
+    ncclResult_t r4 = ncclAllReduce(stats + RLVLA_STAT_N_LOSS_STEPS, stats + RLVLA_STAT_N_LOSS_STEPS, 1,
+                                    ncclDouble, ncclSum, comm->comm, s);
     ncclResult_t r2 = ncclSuccess;
     if (p->mode == RLVLA_ADV_GRPO) {
       float* rg = a.ws.r_global;
@@ -235,7 +265,8 @@ RLVLA_API rlvla_status rlvla_advantages(const rlvla_traj_buffer* buf, const floa
                          comm->comm, s);
     }
     ncclResult_t r3 = ncclGroupEnd();
-    if (r1 != ncclSuccess || r2 != ncclSuccess || r3 != ncclSuccess) return RLVLA_ERR_NCCL;
+    if (r1 != ncclSuccess || r2 != ncclSuccess || r3 != ncclSuccess || r4 != ncclSuccess)
+      return RLVLA_ERR_NCCL;
   }
   st = cuda_status(launch_adv_pass2(a, s));
   if (st != RLVLA_OK) return st;
@@ -248,17 +279,17 @@ RLVLA_API rlvla_status rlvla_logprob_fwd_bwd(const rlvla_logits* x, const int32_
                                              double* stats, void* workspace, size_t ws_bytes,
                                              rlvla_comm comm, void* stream) {
   NvtxRange nvtx_range("rlvla_logprob_fwd_bwd");
-  if (!x || !x->ptr || !target) return RLVLA_ERR_INVALID_ARG;
+  if (!x || ((!x->ptr || !target) && x->rows != 0)) return RLVLA_ERR_INVALID_ARG;
   if (x->dtype != RLVLA_F32 && x->dtype != RLVLA_BF16) return RLVLA_ERR_INVALID_ARG;
   if (x->rows < 0 || x->vocab < 1 || x->ld < x->vocab) return RLVLA_ERR_INVALID_ARG;
   if (fused && grad_logp) return RLVLA_ERR_INVALID_ARG;
   if (grad_logp) {
-    if (!lse || !dlogits) return RLVLA_ERR_INVALID_ARG;
-  } else if (!logp) {
+    if ((!lse || !dlogits) && x->rows != 0) return RLVLA_ERR_INVALID_ARG;
+  } else if (!logp && x->rows != 0) {
     return RLVLA_ERR_INVALID_ARG;
   }
   if (fused) {
-    rlvla_status st = check_ppo_args(fused);
+    rlvla_status st = check_ppo_args(fused, x->rows);
     if (st != RLVLA_OK) return st;
     if (x->rows % fused->a_tok) return RLVLA_ERR_INVALID_ARG;
     if (fused->ratio_level != 0) return RLVLA_ERR_UNSUPPORTED;  // chunk ratio: rlvla_ppo_loss
@@ -267,8 +298,20 @@ RLVLA_API rlvla_status rlvla_logprob_fwd_bwd(const rlvla_logits* x, const int32_
     if (!workspace || ws_bytes < ws_bytes_for(1) || reinterpret_cast<uintptr_t>(workspace) % kAlignWs)
       return RLVLA_ERR_INVALID_ARG;
   }
-  if (x->rows == 0) return RLVLA_OK;
+  const bool want_stats = stats && !grad_logp;
+  if (x->rows == 0 && !want_stats) return RLVLA_OK;
   if (!device_ready()) return RLVLA_ERR_CUDA;
+  if (want_stats && multi_rank(comm) && !uses_p2p(comm) && !comm->comm) return RLVLA_ERR_UNSUPPORTED;
+  if (x->rows == 0) {
+    // no rows on this rank: write this call's (zero or accumulated) statistics and take part
+    // in C3 like the ranks that have rows
+    rlvla_ppo_args f0{};
+    if (fused) f0 = *fused;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    rlvla_status st = stats_only_call(f0, stats, workspace, comm, s);
+    if (st != RLVLA_OK) return st;
+    return sync_check_stats(stats, RLVLA_STAT_N_BAD_TOK, s);
+  }
   LpArgs a{};
   a.x = *x;
   a.target = target;
@@ -298,16 +341,22 @@ RLVLA_API rlvla_status rlvla_ppo_loss(const float* logp, int64_t rows, const int
                                       double* stats, void* workspace, size_t ws_bytes,
                                       rlvla_comm comm, void* stream) {
   NvtxRange nvtx_range("rlvla_ppo_loss");
-  if (!logp || !f || !grad_logp || rows < 0) return RLVLA_ERR_INVALID_ARG;
-  rlvla_status st = check_ppo_args(f);
+  if (!f || rows < 0 || ((!logp || !grad_logp) && rows != 0)) return RLVLA_ERR_INVALID_ARG;
+  rlvla_status st = check_ppo_args(f, rows);
   if (st != RLVLA_OK) return st;
   if (rows % f->a_tok) return RLVLA_ERR_INVALID_ARG;
   if (f->ent_coef != 0.f) return RLVLA_ERR_UNSUPPORTED;  // the entropy bonus needs the logits
+  if (f->ratio_level == 1 && f->kl_coef != 0.f) return RLVLA_ERR_UNSUPPORTED;  // per-token KL vs per-step mean: no reading
   if ((stats || f->ratio_level == 1) &&
       (!workspace || ws_bytes < ws_bytes_for(1) || reinterpret_cast<uintptr_t>(workspace) % kAlignWs))
     return RLVLA_ERR_INVALID_ARG;
-  if (rows == 0) return RLVLA_OK;
+  // chunk ratio with the call's own step count over several ranks: the count is reduced
+  // through `stats`, so they are required
+  const bool implicit_chunk = f->ratio_level == 1 && !(f->tok_denominator > 0.0) && !f->adv_stats;
+  if (implicit_chunk && multi_rank(comm) && !stats) return RLVLA_ERR_INVALID_ARG;
+  if (rows == 0 && !stats) return RLVLA_OK;
   if (!device_ready()) return RLVLA_ERR_CUDA;
+  if (stats && multi_rank(comm) && !uses_p2p(comm) && !comm->comm) return RLVLA_ERR_UNSUPPORTED;
   PpoArgs a{};
   a.logp = logp;
   a.rows = rows;
@@ -320,9 +369,19 @@ RLVLA_API rlvla_status rlvla_ppo_loss(const float* logp, int64_t rows, const int
   // C3 in-kernel over NVLink (token- and chunk-level paths)
   const bool p2p = stats && uses_p2p(comm);
   if (p2p) a.ws.p2p = p2p_desc(comm, P2P_CH_LOSS);
+  // NCCL fallback with the chunk path's own step count: raw sums and counts are allreduced
+  // (slots 6..18), then the scale kernel normalises with the global count
+  a.defer = implicit_chunk && stats && multi_rank(comm) && !p2p;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   st = cuda_status(launch_ppo_loss(a, s));
   if (st != RLVLA_OK) return st;
+  if (a.defer) {
+    st = allreduce_stats(stats + RLVLA_STAT_LOSS, RLVLA_STAT_DENOM + 1 - RLVLA_STAT_LOSS, comm, s);
+    if (st != RLVLA_OK) return st;
+    st = cuda_status(launch_ppo_chunk_scale(a, s));
+    if (st != RLVLA_OK) return st;
+    return sync_check_stats(stats, RLVLA_STAT_N_BAD_TOK, s);
+  }
   if (stats) {
     if (!p2p) st = allreduce_stats(stats + RLVLA_STAT_LOSS, RLVLA_STAT_DENOM - RLVLA_STAT_LOSS, comm, s);
     if (st != RLVLA_OK) return st;
@@ -339,25 +398,32 @@ RLVLA_API rlvla_status rlvla_value_loss(const float* v_new, const float* v_old, 
                                         double* stats, void* workspace, size_t ws_bytes,
                                         rlvla_comm comm, void* stream) {
   NvtxRange nvtx_range("rlvla_value_loss");
-  if (!v_new || !ret || !slot_key || !version || !grad_v || n_steps < 0 || max_staleness < 0)
-    return RLVLA_ERR_INVALID_ARG;
-  if (clip_eps > 0.f && !v_old) return RLVLA_ERR_INVALID_ARG;
+  if (n_steps < 0 || max_staleness < 0) return RLVLA_ERR_INVALID_ARG;
+  if (n_steps > 0 && (!v_new || !ret || !slot_key || !version || !grad_v)) return RLVLA_ERR_INVALID_ARG;
+  if (clip_eps > 0.f && !v_old && n_steps > 0) return RLVLA_ERR_INVALID_ARG;
   if (!(clip_eps == clip_eps)) return RLVLA_ERR_INVALID_ARG;
   if (!workspace || ws_bytes < ws_bytes_for(1) || reinterpret_cast<uintptr_t>(workspace) % kAlignWs)
     return RLVLA_ERR_INVALID_ARG;
   if (reinterpret_cast<uintptr_t>(slot_key) % 8 || (stats && reinterpret_cast<uintptr_t>(stats) % 8))
     return RLVLA_ERR_INVALID_ARG;
-  if (n_steps == 0) return RLVLA_OK;
+  const bool implicit = !(denominator > 0.0);
+  // the call's own N_v over several ranks is reduced through `stats`
+  if (implicit && multi_rank(comm) && !stats) return RLVLA_ERR_INVALID_ARG;
+  if (n_steps == 0 && !stats) return RLVLA_OK;
   if (!device_ready()) return RLVLA_ERR_CUDA;
+  if (stats && multi_rank(comm) && !uses_p2p(comm) && !comm->comm) return RLVLA_ERR_UNSUPPORTED;
   ValueArgs a{v_new, v_old, ret, slot_key, version, n_steps, cur_version, max_staleness, clip_eps,
-              denominator, grad_v, loss_step, stats, carve(workspace)};
+              denominator, grad_v, loss_step, stats, carve(workspace), 0};
   const bool p2p = stats && uses_p2p(comm);
   if (p2p) a.ws.p2p = p2p_desc(comm, P2P_CH_VALUE);
+  a.defer = implicit && stats && multi_rank(comm) && !p2p;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   rlvla_status st = cuda_status(launch_value_loss(a, s));
   if (st != RLVLA_OK || !stats || p2p) return st;
-  return allreduce_stats(stats + RLVLA_STAT_VALUE_LOSS,
-                         RLVLA_STAT_VALUE_DENOM - RLVLA_STAT_VALUE_LOSS, comm, s);
+  st = allreduce_stats(stats + RLVLA_STAT_VALUE_LOSS, RLVLA_STAT_VALUE_DENOM - RLVLA_STAT_VALUE_LOSS,
+                       comm, s);
+  if (st != RLVLA_OK || !a.defer) return st;
+  return cuda_status(launch_value_scale(a, s));
 }
 
 namespace {
@@ -435,21 +501,21 @@ RLVLA_API rlvla_status rlvla_flow_logprob(const rlvla_gauss_chain* c, float* log
                                           void* workspace, size_t ws_bytes, rlvla_comm comm,
                                           void* stream) {
   NvtxRange nvtx_range("rlvla_flow_logprob");
-  if (!c || c->rows < 0 || c->n_steps < 1 || c->dim < 1 || !c->mu || !c->x)
+  if (!c || c->rows < 0 || c->n_steps < 1 || c->dim < 1 || ((!c->mu || !c->x) && c->rows != 0))
     return RLVLA_ERR_INVALID_ARG;
   if (int64_t(c->n_steps) * c->dim > kFlowMaxElems) return RLVLA_ERR_INVALID_ARG;
   if (c->mu_dtype != RLVLA_F32 && c->mu_dtype != RLVLA_BF16) return RLVLA_ERR_INVALID_ARG;
-  if (!c->log_std && !c->sigma_k) return RLVLA_ERR_INVALID_ARG;
+  if (!c->log_std && !c->sigma_k && c->rows != 0) return RLVLA_ERR_INVALID_ARG;
   if (dlog_std && !c->log_std) return RLVLA_ERR_INVALID_ARG;  // no learned ln sigma to differentiate
   if (grad_logp && fused) return RLVLA_ERR_INVALID_ARG;
-  if (!grad_logp && !logp) return RLVLA_ERR_INVALID_ARG;
+  if (!grad_logp && !logp && c->rows != 0) return RLVLA_ERR_INVALID_ARG;
   if (!grad_logp && !fused && (dmu || dlog_std)) return RLVLA_ERR_INVALID_ARG;  // nothing to differentiate
-  if (grad_logp && !dmu && !dlog_std) return RLVLA_ERR_INVALID_ARG;
+  if (grad_logp && !dmu && !dlog_std && c->rows != 0) return RLVLA_ERR_INVALID_ARG;
   if (misaligned(c->mu, c->mu_dtype == RLVLA_BF16 ? 2 : 4) || misaligned(c->x, 4) ||
       (stats && misaligned(stats, 8)))
     return RLVLA_ERR_INVALID_ARG;
   if (fused) {
-    rlvla_status st = check_ppo_args(fused);
+    rlvla_status st = check_ppo_args(fused, c->rows);
     if (st != RLVLA_OK) return st;
     if (fused->a_tok != 1 || fused->ratio_level != 0) return RLVLA_ERR_INVALID_ARG;
   }
@@ -457,8 +523,18 @@ RLVLA_API rlvla_status rlvla_flow_logprob(const rlvla_gauss_chain* c, float* log
     if (!workspace || ws_bytes < ws_bytes_for(1) || misaligned(workspace, kAlignWs))
       return RLVLA_ERR_INVALID_ARG;
   }
-  if (c->rows == 0) return RLVLA_OK;
+  const bool want_stats = stats && !grad_logp;
+  if (c->rows == 0 && !want_stats) return RLVLA_OK;
   if (!device_ready()) return RLVLA_ERR_CUDA;
+  if (want_stats && multi_rank(comm) && !uses_p2p(comm) && !comm->comm) return RLVLA_ERR_UNSUPPORTED;
+  if (c->rows == 0) {  // no rows on this rank: zero / accumulated statistics, C3 as the others
+    rlvla_ppo_args f0{};
+    if (fused) f0 = *fused;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    rlvla_status st = stats_only_call(f0, stats, workspace, comm, s);
+    if (st != RLVLA_OK) return st;
+    return sync_check_stats(stats, RLVLA_STAT_N_BAD_TOK, s);
+  }
   FlowArgs a{};
   a.c = *c;
   a.logp = logp;
@@ -489,63 +565,86 @@ RLVLA_API rlvla_status rlvla_comm_unique_id(void* out) {
 }
 
 namespace {
-// Mailboxes for the in-kernel NVLink reduction: each rank allocates one, the CUDA IPC
-// handles are allgathered over the new NCCL communicator and opened (peer mappings).
-// RLVLA_P2P=0 disables it; any failure leaves the communicator on NCCL collectives.
-void setup_p2p(rlvla_comm c) {
-  const char* env = std::getenv("RLVLA_P2P");
-  if (c->nranks <= 1 || c->nranks > kP2PMaxRanks || (env && env[0] == '0')) return;
+static_assert(sizeof(cudaIpcMemHandle_t) == RLVLA_P2P_HANDLE_BYTES, "IPC handle size");
+
+// this rank's mailbox and call counters, and the IPC handle of the mailbox (no collective)
+bool alloc_mailbox(rlvla_comm c, cudaIpcMemHandle_t* h) {
   bool ok = cudaMalloc(&c->mbox, kP2PMboxBytes) == cudaSuccess &&
             cudaMemset(c->mbox, 0, kP2PMboxBytes) == cudaSuccess &&
             cudaMalloc(&c->seq, kP2PChannels * sizeof(unsigned long long)) == cudaSuccess &&
-            cudaMemset(c->seq, 0, kP2PChannels * sizeof(unsigned long long)) == cudaSuccess;
-  cudaIpcMemHandle_t mine{};
-  ok = ok && cudaIpcGetMemHandle(&mine, c->mbox) == cudaSuccess;
-  void* dev = nullptr;
-  ok = ok && cudaMalloc(&dev, sizeof(cudaIpcMemHandle_t) * size_t(c->nranks + 1)) == cudaSuccess;
-  std::vector<cudaIpcMemHandle_t> all(size_t(c->nranks));
-  if (ok) {
-    uint8_t* d = static_cast<uint8_t*>(dev);
-    const size_t hb = sizeof(cudaIpcMemHandle_t);
-    ok = cudaMemcpy(d + size_t(c->nranks) * hb, &mine, hb, cudaMemcpyHostToDevice) == cudaSuccess &&
-         ncclAllGather(d + size_t(c->nranks) * hb, d, hb, ncclChar, c->comm, nullptr) == ncclSuccess &&
-         cudaDeviceSynchronize() == cudaSuccess &&
-         cudaMemcpy(all.data(), d, hb * size_t(c->nranks), cudaMemcpyDeviceToHost) == cudaSuccess;
-  }
-  if (dev) cudaFree(dev);
-  int opened = 0;
+            cudaMemset(c->seq, 0, kP2PChannels * sizeof(unsigned long long)) == cudaSuccess &&
+            cudaIpcGetMemHandle(h, c->mbox) == cudaSuccess;
+  (void)cudaGetLastError();
+  return ok;
+}
+
+void close_peers(rlvla_comm c) {
+  for (int r = 0; r < c->nranks; ++r)
+    if (r != c->rank && c->peer[r]) cudaIpcCloseMemHandle(c->peer[r]);
+  for (auto& q : c->peer) q = nullptr;
+  (void)cudaGetLastError();
+}
+
+// map every peer's mailbox (all: [nranks] handles in rank order); on failure none stays open
+bool open_peers(rlvla_comm c, const cudaIpcMemHandle_t* all) {
+  bool ok = true;
   for (int r = 0; ok && r < c->nranks; ++r) {
     if (r == c->rank) {
       c->peer[r] = c->mbox;
       continue;
     }
     void* p = nullptr;
-    ok = cudaIpcOpenMemHandle(&p, all[size_t(r)], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
-    c->peer[r] = static_cast<uint8_t*>(p);
-    opened += ok;
+    ok = cudaIpcOpenMemHandle(&p, all[r], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+    c->peer[r] = ok ? static_cast<uint8_t*>(p) : nullptr;
   }
-  // every rank must agree: a rank that failed to map makes all of them use NCCL
+  if (!ok) close_peers(c);
+  (void)cudaGetLastError();
+  return ok;
+}
+
+// one record per rank in the NCCL handle exchange: the handle and whether the rank has one
+struct HandleRec {
+  cudaIpcMemHandle_t h;
+  int32_t ok;
+  int32_t pad[15];
+};
+size_t stage_bytes(int nranks) { return sizeof(HandleRec) * size_t(nranks + 1) + sizeof(int); }
+
+// Mailboxes for the in-kernel NVLink reduction over an NCCL communicator: the handles are
+// allgathered over it and opened (peer mappings). `stage` is device memory allocated before
+// the communicator existed, so every rank enters the same two collectives (the allgather,
+// then a min-vote) whatever its local result; a rank that failed to allocate or map makes
+// every rank keep the NCCL collectives. RLVLA_P2P=0 disables it (on every rank).
+void setup_p2p(rlvla_comm c, uint8_t* stage) {
+  const char* env = std::getenv("RLVLA_P2P");
+  if (c->nranks <= 1 || c->nranks > kP2PMaxRanks || (env && env[0] == '0')) return;
+  HandleRec mine{};
+  mine.ok = alloc_mailbox(c, &mine.h) ? 1 : 0;
+  const size_t rb = sizeof(HandleRec);
+  uint8_t* recv = stage;
+  uint8_t* send = stage + size_t(c->nranks) * rb;
+  int* vote = reinterpret_cast<int*>(stage + size_t(c->nranks + 1) * rb);
+  if (cudaMemcpy(send, &mine, rb, cudaMemcpyHostToDevice) != cudaSuccess) mine.ok = 0;
+  std::vector<HandleRec> all(size_t(c->nranks));
+  bool ok = ncclAllGather(send, recv, rb, ncclChar, c->comm, nullptr) == ncclSuccess &&
+            cudaDeviceSynchronize() == cudaSuccess &&
+            cudaMemcpy(all.data(), recv, rb * size_t(c->nranks), cudaMemcpyDeviceToHost) == cudaSuccess;
+  for (int r = 0; ok && r < c->nranks; ++r) ok = all[size_t(r)].ok == 1;
+  if (ok) {
+    std::vector<cudaIpcMemHandle_t> h(size_t(c->nranks));
+    for (int r = 0; r < c->nranks; ++r) h[size_t(r)] = all[size_t(r)].h;
+    ok = open_peers(c, h.data());
+  }
+  // every rank must agree: a rank that failed makes all of them use NCCL
   int flag = ok ? 1 : 0;
-  int* dflag = nullptr;
-  if (cudaMalloc(&dflag, sizeof(int)) == cudaSuccess) {
-    cudaMemcpy(dflag, &flag, sizeof(int), cudaMemcpyHostToDevice);
-    if (ncclAllReduce(dflag, dflag, 1, ncclInt, ncclMin, c->comm, nullptr) == ncclSuccess &&
-        cudaDeviceSynchronize() == cudaSuccess)
-      cudaMemcpy(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost);
-    else
-      flag = 0;
-    cudaFree(dflag);
-  } else {
+  const bool voted = cudaMemcpy(vote, &flag, sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess;
+  if (ncclAllReduce(vote, vote, 1, ncclInt, ncclMin, c->comm, nullptr) != ncclSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess || !voted ||
+      cudaMemcpy(&flag, vote, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
     flag = 0;
-  }
   (void)cudaGetLastError();
   c->p2p = flag == 1;
-  if (!c->p2p) {
-    for (int r = 0; r < c->nranks; ++r)
-      if (r != c->rank && c->peer[r]) cudaIpcCloseMemHandle(c->peer[r]);
-    for (auto& q : c->peer) q = nullptr;
-    (void)opened;
-  }
+  if (!c->p2p) close_peers(c);
 }
 }  // namespace
 
@@ -556,27 +655,66 @@ RLVLA_API rlvla_status rlvla_comm_init(const void* id, int32_t nranks, int32_t r
   if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks) return RLVLA_ERR_INVALID_ARG;
   ncclUniqueId uid;
   std::memcpy(&uid, id, sizeof(uid));
+  // the handle-exchange staging buffer exists before the communicator does: a rank that
+  // cannot allocate it fails here, like a failed NCCL init, not inside a collective
+  uint8_t* stage = nullptr;
+  if (nranks > 1 && cudaMalloc(&stage, stage_bytes(nranks)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return RLVLA_ERR_CUDA;
+  }
   rlvla_comm c = new rlvla_comm_s{};
   c->nranks = nranks;
   c->rank = rank;
   if (ncclCommInitRank(&c->comm, nranks, uid, rank) != ncclSuccess) {
+    if (stage) cudaFree(stage);
     delete c;
     return RLVLA_ERR_NCCL;
   }
-  setup_p2p(c);  // best effort: without it the collectives stay on NCCL
+  if (stage) {
+    setup_p2p(c, stage);  // best effort: without it the collectives stay on NCCL
+    cudaFree(stage);
+  }
   *out = c;
+  return RLVLA_OK;
+}
+
+RLVLA_API rlvla_status rlvla_comm_init_p2p(int32_t nranks, int32_t rank, void* out_handle,
+                                           rlvla_comm* out) {
+  if (!out_handle || !out || nranks < 1 || nranks > kP2PMaxRanks || rank < 0 || rank >= nranks)
+    return RLVLA_ERR_INVALID_ARG;
+  if (!device_ready()) return RLVLA_ERR_CUDA;
+  rlvla_comm c = new rlvla_comm_s{};
+  c->nranks = nranks;
+  c->rank = rank;
+  cudaIpcMemHandle_t h{};
+  if (nranks > 1 && !alloc_mailbox(c, &h)) {
+    if (c->mbox) cudaFree(c->mbox);
+    if (c->seq) cudaFree(c->seq);
+    delete c;
+    return RLVLA_ERR_CUDA;
+  }
+  std::memcpy(out_handle, &h, sizeof(h));
+  *out = c;
+  return RLVLA_OK;
+}
+
+RLVLA_API rlvla_status rlvla_comm_connect_p2p(rlvla_comm c, const void* all_handles) {
+  if (!c || !all_handles || c->comm) return RLVLA_ERR_INVALID_ARG;
+  if (c->nranks <= 1) return RLVLA_OK;
+  if (c->p2p) return RLVLA_ERR_INVALID_ARG;  // already connected
+  std::vector<cudaIpcMemHandle_t> h(size_t(c->nranks));
+  std::memcpy(h.data(), all_handles, sizeof(cudaIpcMemHandle_t) * size_t(c->nranks));
+  if (!open_peers(c, h.data())) return RLVLA_ERR_CUDA;
+  c->p2p = true;
   return RLVLA_OK;
 }
 
 RLVLA_API rlvla_status rlvla_comm_destroy(rlvla_comm c) {
   if (!c) return RLVLA_OK;
-  if (c->p2p) {
-    for (int r = 0; r < c->nranks; ++r)
-      if (r != c->rank && c->peer[r]) cudaIpcCloseMemHandle(c->peer[r]);
-  }
+  close_peers(c);
   if (c->mbox) cudaFree(c->mbox);
   if (c->seq) cudaFree(c->seq);
-  ncclResult_t r = ncclCommDestroy(c->comm);
+  const ncclResult_t r = c->comm ? ncclCommDestroy(c->comm) : ncclSuccess;
   delete c;
   return r == ncclSuccess ? RLVLA_OK : RLVLA_ERR_NCCL;
 }

@@ -370,8 +370,10 @@ struct PpoArgs {
   float* loss_tok;
   double* stats;
   Workspace ws;
+  int defer;  // chunk path, implicit N over NCCL: raw sums out, scale after the allreduce
 };
 cudaError_t launch_ppo_loss(const PpoArgs& a, cudaStream_t s);
+cudaError_t launch_ppo_chunk_scale(const PpoArgs& a, cudaStream_t s);
 
 struct ValueArgs {
   const float* v_new;
@@ -387,8 +389,10 @@ struct ValueArgs {
   float* loss_step;
   double* stats;
   Workspace ws;
+  int defer;  // implicit N_v over NCCL: raw sums out, scale after the allreduce
 };
 cudaError_t launch_value_loss(const ValueArgs& a, cudaStream_t s);
+cudaError_t launch_value_scale(const ValueArgs& a, cudaStream_t s);
 
 struct BatchOfferArgs {
   rlvla_batch_queue q;

@@ -60,42 +60,70 @@ __global__ void __launch_bounds__(256) value_loss_kernel(ValueArgs a) {
   }
   __shared__ double tot[3];
   if (last_block_reduce(a.ws.ctrl + CTRL_VALUE, a.ws.partials, 3, tot)) {
+    // implicit N_v: the raw sums are reduced over the ranks first (in-kernel), so N_v is the
+    // global step count; with the NCCL fallback (defer) the raw sums go out and the scale
+    // kernel finishes after the host allreduce
+    if (!explicit_n && a.stats && a.ws.p2p.nranks > 1) p2p_exchange(tot, 3, a.ws.p2p);
+    __syncthreads();
     const double N = explicit_n ? a.denominator : tot[2];
     const double inv = N > 0.0 ? 1.0 / N : 0.0;
     __syncthreads();
     if (threadIdx.x == 0) {
       *value_scratch(a) = inv;
-      tot[0] *= inv;  // this rank's share of the loss, as the NCCL path reduces it
+      if (!a.defer) tot[0] *= inv;  // this rank's share of the loss, as the NCCL path reduces it
     }
     __syncthreads();
-    if (a.stats && a.ws.p2p.nranks > 1) p2p_exchange(tot, 3, a.ws.p2p);  // in-kernel (NVLink)
+    if (explicit_n && a.stats && a.ws.p2p.nranks > 1) p2p_exchange(tot, 3, a.ws.p2p);  // in-kernel (NVLink)
     if (threadIdx.x == 0 && a.stats) {
       a.stats[RLVLA_STAT_VALUE_LOSS] = tot[0];
       a.stats[RLVLA_STAT_N_VALUE_CLIPPED] = tot[1];
       a.stats[RLVLA_STAT_N_VALUE_STEPS] = tot[2];
-      a.stats[RLVLA_STAT_VALUE_DENOM] = N;
+      a.stats[RLVLA_STAT_VALUE_DENOM] = a.defer ? 0.0 : N;
     }
   }
 }
 
+// second pass when N_v is the call's own count: scale the gradients by 1/N_v; with defer
+// (NCCL fallback) N_v is the allreduced count in stats and CTA 0 normalises the loss slot
 __global__ void __launch_bounds__(256) value_scale_kernel(ValueArgs a) {
-  const float fi = float(*value_scratch(a));
+  float fi;
+  if (a.defer) {
+    const double N = a.stats[RLVLA_STAT_N_VALUE_STEPS];
+    const double inv = N > 0.0 ? 1.0 / N : 0.0;
+    fi = float(inv);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.stats[RLVLA_STAT_VALUE_LOSS] *= inv;
+      a.stats[RLVLA_STAT_VALUE_DENOM] = N;
+    }
+  } else {
+    fi = float(*value_scratch(a));
+  }
   for (int64_t s = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < a.n;
        s += int64_t(gridDim.x) * blockDim.x)
     a.grad_v[s] *= fi;
 }
 
+int value_grid(int64_t n) {
+  const int sms = device_info().sm_count;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > int64_t(sms) * 4) blocks = int64_t(sms) * 4;
+  return blocks < 1 ? 1 : int(blocks);
+}
+
 }  // namespace
 
+// n == 0 still launches one CTA when statistics are requested (this rank's zeros take part
+// in the cross-rank reduction)
 cudaError_t launch_value_loss(const ValueArgs& a, cudaStream_t s) {
-  if (a.n <= 0) return cudaSuccess;
-  const int sms = device_info().sm_count;
-  int64_t blocks = (a.n + 255) / 256;
-  if (blocks > int64_t(sms) * 4) blocks = int64_t(sms) * 4;
-  value_loss_kernel<<<int(blocks), 256, 0, s>>>(a);
+  if (a.n <= 0 && a.stats == nullptr) return cudaSuccess;
+  value_loss_kernel<<<value_grid(a.n), 256, 0, s>>>(a);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess || a.denominator > 0.0) return e;
-  value_scale_kernel<<<int(blocks), 256, 0, s>>>(a);
+  if (e != cudaSuccess || a.denominator > 0.0 || a.defer) return e;
+  return launch_value_scale(a, s);
+}
+
+cudaError_t launch_value_scale(const ValueArgs& a, cudaStream_t s) {
+  value_scale_kernel<<<value_grid(a.n), 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 

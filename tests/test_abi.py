@@ -17,14 +17,14 @@ def L():
 
 def test_exports_every_header_symbol(L):
     names = A.header_functions()
-    assert len(names) == 16
+    assert len(names) == 18
     for n in names:
         assert hasattr(L, n), n
     assert set(names) == set(A._SIGS)
 
 
 def test_host_only_calls(L):
-    assert L.rlvla_abi_version() == 1
+    assert L.rlvla_abi_version() == 2
     assert L.rlvla_nccl_version() >= 22800
     for s in range(6):
         assert L.rlvla_status_string(s)
@@ -136,6 +136,27 @@ def test_ppo_loss_validation(L):
     assert L.rlvla_ppo_loss(FAKE, 6, None, ctypes.byref(f), FAKE, None, None, None, 0, None, None) == A.ERR_INVALID_ARG
     f.eps_low = 1.5
     assert L.rlvla_ppo_loss(FAKE, 8, None, ctypes.byref(f), FAKE, None, None, None, 0, None, None) == A.ERR_INVALID_ARG
+    f.eps_low = 0.2
+    # chunk ratio (R21): a KL term has no step-level reading; accumulate needs N_steps up front
+    f.ratio_level, f.logp_ref, f.kl_coef = 1, FAKE, 0.1
+    ws_n = L.rlvla_workspace_bytes(0, 1, 1)
+    call = lambda: L.rlvla_ppo_loss(FAKE, 8, None, ctypes.byref(f), FAKE, None, None, 0x100000, ws_n, None, None)  # noqa: E731
+    assert call() == A.ERR_UNSUPPORTED
+    f.kl_coef, f.tok_denominator, f.accumulate = 0.0, 0.0, 1
+    assert call() == A.ERR_INVALID_ARG
+    # rows = 0 without stats is a no-op even with NULL arrays (a rank without rows)
+    f0 = A.c_ppo_args(None, None, None, None, None, 4, 100, 1, 0.2, 0.2, 0.0, 1.0, None, None, None)
+    assert L.rlvla_ppo_loss(None, 0, None, ctypes.byref(f0), None, None, None, None, 0, None, None) == A.OK
+
+
+def test_p2p_only_comm_without_gpu(L):
+    h = ctypes.c_void_p()
+    buf = (ctypes.c_ubyte * A.P2P_HANDLE_BYTES)()
+    assert L.rlvla_comm_init_p2p(9, 0, buf, ctypes.byref(h)) == A.ERR_INVALID_ARG   # > 8 ranks
+    assert L.rlvla_comm_init_p2p(2, 2, buf, ctypes.byref(h)) == A.ERR_INVALID_ARG   # rank >= n
+    assert L.rlvla_comm_init_p2p(2, 0, None, ctypes.byref(h)) == A.ERR_INVALID_ARG
+    assert L.rlvla_comm_init_p2p(2, 0, buf, ctypes.byref(h)) == A.ERR_CUDA          # no device here
+    assert L.rlvla_comm_connect_p2p(None, buf) == A.ERR_INVALID_ARG
 
 
 def test_batcher_validation(L):

@@ -20,19 +20,29 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("p2p", ["1", "0"])
-@pytest.mark.parametrize("n", [2, 4])
-def test_nccl_multigpu_parity(n, p2p):
+@pytest.mark.parametrize("n,mode", [(2, "p2p"), (2, "nccl"), (4, "p2p"), (4, "nccl"),
+                                    (4, "p2p-only"), (8, "p2p-only")])
+def test_multigpu_parity(n, mode):
     """The loss statistics reduced in-kernel over NVLink peer memory (RLVLA_P2P=1, the
-    default) and through NCCL (RLVLA_P2P=0) both match the oracle."""
-    if torch.cuda.device_count() < n:
+    default), through NCCL (RLVLA_P2P=0), and with the P2P-only communicator (no NCCL; a gloo
+    group exchanges the IPC handles, ranks round-robin over the GPUs, so 8 ranks run on 4
+    GPUs at the mailbox's full 8-rank capacity) all match the oracle."""
+    ndev = torch.cuda.device_count()
+    if mode == "p2p-only":
+        if ndev < 2 or n > 4 * ndev:
+            pytest.skip(f"needs >= 2 GPUs and <= 4 ranks per GPU (have {ndev})")
+    elif ndev < n:
         pytest.skip(f"needs {n} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tools", "mgpu_parity.py")]
-    env = dict(os.environ, RLVLA_P2P=p2p)
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    env = dict(os.environ, RLVLA_P2P="0" if mode == "nccl" else "1",
+               RLVLA_MGPU_MODE="p2p-only" if mode == "p2p-only" else "nccl")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "MGPU PARITY OK" in r.stdout
-    if p2p == "0":
+    print(r.stdout.strip().splitlines()[-1])
+    if mode == "nccl":
         assert "in-kernel-p2p=False" in r.stdout
+    else:
+        assert "in-kernel-p2p=True" in r.stdout

@@ -1,8 +1,11 @@
-"""World-size-2 (gloo, CPU) test of the data-parallel sharding the C ABI implements with
-NCCL: contiguous env shards, records routed to their owner rank, C1 (advantage-statistics
-allreduce), C2 (GRPO returns allgather, groups spanning ranks), C3 (loss-statistics
-allreduce). The sharded computation (oracle arithmetic + host sharding helpers + the
-collectives) must equal the unsharded one."""
+"""World-size 2 and 8 (gloo, CPU) tests of the data-parallel sharding the C ABI implements
+over NVLink / NCCL: contiguous env shards, records routed to their owner rank, C1
+(advantage-statistics allreduce), C2 (GRPO returns allgather, groups spanning ranks), C3
+(loss-statistics allreduce). The sharded computation (oracle arithmetic + host sharding
+helpers + the collectives) must equal the unsharded one. Cases: tiny at world 2, and the
+shapes of BASELINE configs 4 (ManiSkill PPO+GAE with whitening, 8 ranks) and 5 (GRPO groups
+of 8 interleaved so every group has one member on each of the 8 ranks) with a small
+vocabulary so the oracle finishes in seconds."""
 import os
 import socket
 
@@ -18,7 +21,16 @@ from oracle import path as O_path
 from oracle import scatter as O_sc
 from paper_2602_05765_b200 import sharding
 
-WORLD = 2
+CASES = {
+    "tiny_w2": (2, lambda: synth.scaled(synth.CONFIGS["tiny"], n_env=16, group_size=4,
+                                        interleave_groups=True, faults=False)),
+    # config 4 shape: 1024 envs x 80 steps, chunk 8 -> 8 envs per rank x 10 steps x 56 tokens
+    "maniskill_w8": (8, lambda: synth.scaled(synth.CONFIGS["maniskill_ppo_gae"], n_env=64,
+                                             vocab=64, dtype="f32")),
+    # config 5 shape: GRPO groups of 8 spanning all 8 ranks (g(e) = e mod E/G)
+    "grpo_span_w8": (8, lambda: synth.scaled(synth.CONFIGS["grpo_span"], n_env=64, n_es=32,
+                                             vocab=64, dtype="f32")),
+}
 
 
 def _free_port():
@@ -29,9 +41,8 @@ def _free_port():
     return p
 
 
-def _case():
-    cfg = synth.scaled(synth.CONFIGS["tiny"], n_env=16, group_size=4, interleave_groups=True,
-                       faults=False)
+def _case(name):
+    cfg = CASES[name][1]()
     traj = synth.make_trajectories(cfg)
     rec = synth.make_records(traj, 0, cfg.n_env)         # global env ids, arrival order
     x = synth.gen_logits(cfg, traj, 0, cfg.n_env).double().numpy()
@@ -57,6 +68,7 @@ def _pipeline(cfg, traj, rec, x, lo, hi, idx, local_env, allreduce, allgather):
     R_loc = O_adv.episode_return(buf["reward"], valid)
     R_glob = allgather(R_loc)
     A_grpo = O_adv.grpo_step_adv(O_adv.grpo(R_glob, traj.group_id)[lo:hi], valid)
+    adv_loss = A_grpo if cfg.adv_mode == "grpo" else None
     # S2 GAE + global whitening: (n, sum A, sum A^2) allreduce (C1)
     a_gae, _ = O_adv.gae(buf["reward"], buf["value"], buf["done"], valid,
                          traj.last_value[lo:hi], 0.99, 0.95)
@@ -64,8 +76,8 @@ def _pipeline(cfg, traj, rec, x, lo, hi, idx, local_env, allreduce, allgather):
     a_w = O_adv.whiten(a_gae, valid, 1e-8, stats=tuple(st))
     c = O_adv.step_counts(valid, buf["version"], buf["tokens"], synth.CUR_VERSION, 1)
     n_tok = allreduce(np.array([c["n_tok"]], np.float64))[0]
-    # S3+S4 on own rows with the global N_tok; loss stats allreduce (C3)
-    tv = O_path.token_view(buf, A_grpo, A, synth.CUR_VERSION)
+    # S3+S4 on own rows with the global N_tok (the config's advantages); loss stats (C3)
+    tv = O_path.token_view(buf, a_w if adv_loss is None else adv_loss, A, synth.CUR_VERSION)
     rows = np.arange(E_r * T * A)
     out = O_path.loss_and_grad(x[lo * T * A:hi * T * A], tv, n_tok=n_tok, rows=rows)
     keys = ["loss", "n_clipped", "kl_k3_sum", "entropy_sum", "ratio_sum", "n_loss_tok"]
@@ -73,12 +85,13 @@ def _pipeline(cfg, traj, rec, x, lo, hi, idx, local_env, allreduce, allgather):
     return dict(grpo=A_grpo, gae_w=a_w, n_tok=n_tok, loss=loss, dx=out["dx"], buf=buf)
 
 
-def _worker(rank, port, q):
+def _worker(rank, port, q, name):
+    WORLD = CASES[name][0]
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
     try:
-        cfg, traj, rec, x = _case()
+        cfg, traj, rec, x = _case(name)
         lo, hi = sharding.env_range(cfg.n_env, WORLD, rank)
         idx, local_env = sharding.route_records(rec.env_id, cfg.n_env, WORLD, rank)
 
@@ -99,18 +112,20 @@ def _worker(rank, port, q):
         dist.destroy_process_group()
 
 
-def test_sharded_equals_unsharded_world2():
+@pytest.mark.parametrize("name", list(CASES))
+def test_sharded_equals_unsharded(name):
+    WORLD = CASES[name][0]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(WORLD)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, name)) for r in range(WORLD)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=240) for _ in range(WORLD))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    cfg, traj, rec, x = _case()
+    cfg, traj, rec, x = _case(name)
     ident = lambda v: np.asarray(v, np.float64)  # noqa: E731
     full = _pipeline(cfg, traj, rec, x, 0, cfg.n_env, np.arange(rec.n), rec.env_id, ident, ident)
     E_r = cfg.n_env // WORLD
@@ -121,10 +136,16 @@ def test_sharded_equals_unsharded_world2():
         np.testing.assert_allclose(res[r]["gae_w"], full["gae_w"][sl], rtol=1e-12, atol=1e-12)
         assert res[r]["n_tok"] == full["n_tok"]
         np.testing.assert_allclose(res[r]["loss"], full["loss"], rtol=1e-12, atol=1e-15)
-        np.testing.assert_array_equal(res[r]["dx"], full["dx"][r * E_r * T * A:(r + 1) * E_r * T * A])
-    # groups really span the ranks
-    g = traj.group_id
-    assert all(len({e // E_r for e in np.nonzero(g == k)[0]}) == WORLD for k in np.unique(g))
+        dx_full = full["dx"][r * E_r * T * A:(r + 1) * E_r * T * A]
+        if cfg.adv_mode == "grpo":      # rank-invariant advantages => bit-identical rows
+            np.testing.assert_array_equal(res[r]["dx"], dx_full)
+        else:                           # whitened: (mu, sigma) differ by the sum order
+            np.testing.assert_allclose(res[r]["dx"], dx_full, rtol=1e-12, atol=1e-300)
+    # groups really span the ranks (GRPO configs)
+    if cfg.group_size:
+        g = traj.group_id
+        assert all(len({e // E_r for e in np.nonzero(g == k)[0]}) == min(WORLD, cfg.group_size)
+                   for k in np.unique(g))
 
 
 def test_route_records_partitions_stream():

@@ -157,7 +157,7 @@ def test_step_counts_brute_force():
     version = 10 - rng.integers(-1, 4, size=(E, T))
     tokens = rng.integers(-1, 5, size=(E, T, Atok))
     c = A.step_counts(valid, version, tokens, 10, 1)
-    nv = nt = ns = nb = 0
+    nv = nt = ns = nb = nls = 0
     for e in range(E):
         for t in range(T):
             if not valid[e, t]:
@@ -169,5 +169,7 @@ def test_step_counts_brute_force():
             elif lag > 1:
                 ns += 1
             else:
-                nt += sum(1 for a in range(Atok) if tokens[e, t, a] >= 0)
-    assert c == dict(n_valid=nv, n_tok=nt, n_stale=ns, n_bad=nb)
+                k = sum(1 for a in range(Atok) if tokens[e, t, a] >= 0)
+                nt += k
+                nls += k > 0
+    assert c == dict(n_valid=nv, n_tok=nt, n_stale=ns, n_bad=nb, n_loss_steps=nls)

@@ -114,31 +114,67 @@ def test_entropy_bonus_gradient_pins():
     assert L.entropy_bonus_grad(x2, f2["lse"], f2["entropy"], [1.0])[0, 2] == 0.0
 
 
-def test_chunk_ratio_matches_autograd_and_reduces_to_token_level():
+@pytest.mark.parametrize("prox,cap,dual", [(False, 0.0, 0.0), (True, 0.0, 0.0), (True, 1.05, 0.0),
+                                            (False, 0.0, 1.3), (True, 1.1, 1.3)])
+def test_chunk_ratio_matches_autograd_and_reduces_to_token_level(prox, cap, dual):
     rng = np.random.default_rng(4)
-    S, Atok = 12, 5
+    S, Atok = 40, 5
     R = S * Atok
     logp = rng.normal(-3, 0.5, R)
-    lb = logp - rng.normal(0, 0.05, R)
+    lb = logp - rng.normal(0, 0.08, R)
+    lpp = lb + rng.normal(0, 0.03, R)
     adv = rng.normal(size=S)
     m = rng.random(R) > 0.15
     st = np.arange(R) // Atok
-    o = O.ppo_loss_chunk(logp, lb, adv, m, st, S)
+    kw = dict(logp_prox=lpp if prox else None, is_cap=cap, dual_clip=dual)
+    o = O.ppo_loss_chunk(logp, lb, adv, m, st, S, **kw)
+    assert not o["near_tie_step"].any()
+    if dual:
+        assert o["dual"].any()                     # the dual branch is exercised
+    if cap:
+        assert (o["w_step"] == cap).any()          # the cap binds somewhere
     t = torch.tensor(logp, requires_grad=True)
-    lr = torch.zeros(S, dtype=torch.float64).index_add(0, torch.tensor(st), (t - torch.tensor(lb)) * torch.tensor(m, dtype=torch.float64))
+    mt = torch.tensor(m, dtype=torch.float64)
+    base = torch.tensor(lpp if prox else lb)
+    lr = torch.zeros(S, dtype=torch.float64).index_add(0, torch.tensor(st), (t - base) * mt)
     rho = torch.exp(lr)
+    w = torch.ones(S, dtype=torch.float64)
+    if prox:                                       # detached importance weight (R12)
+        w = torch.exp(torch.zeros(S, dtype=torch.float64).index_add(
+            0, torch.tensor(st), torch.tensor(lpp - lb) * mt))
+        if cap:
+            w = torch.clamp(w, max=cap)
     At = torch.tensor(adv)
     J = torch.minimum(rho * At, torch.clamp(rho, 0.8, 1.2) * At)
+    if dual:
+        J = torch.where(At < 0, torch.maximum(J, dual * At), J)
     ms = torch.tensor(o["mask_step"], dtype=torch.float64)
-    loss = -(J * ms).sum() / ms.sum()
+    loss = -(w * J * ms).sum() / ms.sum()
     loss.backward()
     assert abs(loss.item() - o["stats"]["loss"]) < 1e-13
     np.testing.assert_allclose(o["grad"], t.grad.numpy() * m, atol=1e-15)
-    # one token per step == the token-level surrogate
-    o1 = O.ppo_loss_chunk(logp[:S], lb[:S], adv, np.ones(S, bool), np.arange(S), S)
-    o2 = O.ppo_loss(logp[:S], lb[:S], adv, np.ones(S, bool), np.zeros(S, int))
-    np.testing.assert_allclose(o1["grad"], o2["grad"], rtol=1e-14)
+    # one token per step == the token-level surrogate (same knobs)
+    o1 = O.ppo_loss_chunk(logp[:S], lb[:S], adv, np.ones(S, bool), np.arange(S), S,
+                          logp_prox=lpp[:S] if prox else None, is_cap=cap, dual_clip=dual)
+    o2 = O.ppo_loss(logp[:S], lb[:S], adv, np.ones(S, bool), np.zeros(S, int),
+                    logp_prox=lpp[:S] if prox else None, is_cap=cap, dual_clip=dual)
+    np.testing.assert_allclose(o1["grad"], o2["grad"], rtol=1e-14, atol=1e-300)
     assert abs(o1["stats"]["loss"] - o2["stats"]["loss"]) < 1e-14
+    assert o1["stats"]["n_dual_clipped"] == o2["stats"]["n_dual_clipped"]
+
+
+def test_chunk_decoupled_with_prox_equal_behav_is_standard():
+    rng = np.random.default_rng(9)
+    S, Atok = 30, 4
+    R = S * Atok
+    logp = rng.normal(-3, 0.5, R)
+    lb = logp - rng.normal(0, 0.1, R)
+    adv = rng.normal(size=S)
+    m = rng.random(R) > 0.1
+    st = np.arange(R) // Atok
+    a = O.ppo_loss_chunk(logp, lb, adv, m, st, S)
+    b = O.ppo_loss_chunk(logp, lb, adv, m, st, S, logp_prox=lb)
+    assert np.array_equal(a["grad"], b["grad"]) and a["stats"] == b["stats"]
 
 
 def test_value_loss_matches_autograd_and_special_cases():

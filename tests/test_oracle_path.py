@@ -134,27 +134,31 @@ def test_gae_path_ignores_junk_and_whitens_over_filled_steps():
 # ---------------------------------------------------------------------------------------
 
 def test_step_counts_closed_form():
-    """E x T x A = 4 x 5 x 3, all filled at lag 0 with every target >= 0 => n_tok = 60; then
-    k = 2 steps at lag 2 (stale), 1 step at lag -1 (bad), 4 targets = -1 on ok steps, and
-    2 unfilled steps (one of them at lag 5 and one with targets -1: both ignored)."""
+    """E x T x A = 4 x 5 x 3, all filled at lag 0 with every target >= 0 => n_tok = 60 and
+    20 loss steps; then 2 steps at lag 2 (stale), 1 step at lag -1 (bad), 4 targets = -1 on
+    ok steps, one ok step with all 3 targets = -1 (no loss step), and 2 unfilled steps (one
+    of them at lag 5 and one with targets -1: both ignored)."""
     E, T, At, cur = 4, 5, 3, 100
     valid = np.ones((E, T), bool)
     version = np.full((E, T), cur)
     tokens = np.zeros((E, T, At), np.int64)
-    assert A.step_counts(valid, version, tokens, cur, 1) == dict(n_valid=20, n_tok=60,
-                                                                 n_stale=0, n_bad=0)
+    assert A.step_counts(valid, version, tokens, cur, 1) == dict(
+        n_valid=20, n_tok=60, n_stale=0, n_bad=0, n_loss_steps=20)
     version[0, 1] = version[2, 3] = cur - 2       # stale (lag 2 > eta = 1)
     version[1, 0] = cur + 1                       # future (lag -1)
     version[3, 4] = cur - 1                       # lag 1 == eta: still counted
     tokens[0, 0, 0] = tokens[0, 0, 2] = tokens[1, 1, 1] = tokens[3, 4, 0] = -1
+    tokens[2, 0, :] = -1                          # an ok step without a usable token
     valid[2, 2] = valid[3, 0] = False
     version[2, 2] = cur - 5
     tokens[3, 0, :] = -1
-    # n_valid = 20 - 2 unfilled = 18; n_tok = 3 * (18 - 2 stale - 1 bad) - 4 ignored = 41
-    assert A.step_counts(valid, version, tokens, cur, 1) == dict(n_valid=18, n_tok=41,
-                                                                 n_stale=2, n_bad=1)
-    # eta = 2 admits the two lag-2 steps: n_tok = 3 * 17 - 4 = 47
-    assert A.step_counts(valid, version, tokens, cur, 2)["n_tok"] == 47
+    # n_valid = 20 - 2 unfilled = 18; ok steps = 18 - 2 stale - 1 bad = 15;
+    # n_tok = 3 * 15 - 4 - 3 = 38; loss steps = 15 - 1 = 14
+    assert A.step_counts(valid, version, tokens, cur, 1) == dict(
+        n_valid=18, n_tok=38, n_stale=2, n_bad=1, n_loss_steps=14)
+    # eta = 2 admits the two lag-2 steps: n_tok = 3 * 17 - 7 = 44, 16 loss steps
+    c2 = A.step_counts(valid, version, tokens, cur, 2)
+    assert (c2["n_tok"], c2["n_loss_steps"]) == (44, 16)
 
 
 def test_token_view_row_to_step_and_lag_sign():

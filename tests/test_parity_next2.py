@@ -157,34 +157,111 @@ def test_ppo_loss_token_variants(var):
     assert abs(s[6] - o["stats"]["loss"]) <= 1e-5 * abs(o["stats"]["loss"]) + 1e-7
 
 
-def test_ppo_loss_chunk_ratio():
-    P = _P()
-    S, A = 300, 56
+def _chunk_case(S=300, A=56, seed=2):
+    rng = np.random.default_rng(seed)
     R = S * A
-    rng = np.random.default_rng(2)
     logp = rng.normal(-4, 1, R).astype(np.float32)
     lb = (logp - rng.normal(0, 0.004, R)).astype(np.float32)     # step ratios ~ e^{N(0, 0.03)}
+    lpp = (lb + rng.normal(0, 0.003, R)).astype(np.float32)
     t = np.where(rng.random(R) < 0.03, -1, 5).astype(np.int32)
+    t[7 * A:8 * A] = -1                                           # a step with no usable token
     adv = rng.normal(size=S).astype(np.float32)
     ver = (100 - rng.choice([0, 1, 2], size=S, p=[0.7, 0.2, 0.1])).astype(np.int32)
     key = np.where(rng.random(S) < 0.95, 3, 0).astype(np.int64)
+    lag = np.repeat(100 - ver.astype(np.int64), A)
+    m = np.repeat(key != 0, A) & (t >= 0) & (lag >= 0) & (lag <= 1)
+    return R, logp, lb, lpp, t, adv, ver, key, m
+
+
+CHUNK_VARIANTS = [dict(), dict(prox=True), dict(prox=True, is_cap=1.01), dict(dual_clip=1.02),
+                  dict(prox=True, is_cap=1.01, dual_clip=1.02)]
+
+
+@pytest.mark.parametrize("den", ["explicit", "adv_stats", "implicit"])
+@pytest.mark.parametrize("var", CHUNK_VARIANTS)
+def test_ppo_loss_chunk_ratio(var, den):
+    """Chunk-level ratio (R21) incl. decoupled weights, the cap and dual clip at step level;
+    N_steps explicit, from a stats vector's N_LOSS_STEPS slot, or the call's own count."""
+    P = _P()
+    S, A = 300, 56
+    R, logp, lb, lpp, t, adv, ver, key, m = _chunk_case(S, A)
+    prox = var.get("prox", False)
+    kw = {k: v for k, v in var.items() if k != "prox"}
+    o_kw = dict(logp_prox=lpp if prox else None, is_cap=var.get("is_cap", 0.0),
+                dual_clip=var.get("dual_clip", 0.0))
+    o_own = O_ppo.ppo_loss_chunk(logp, lb, adv, m, np.arange(R) // A, S, **o_kw)
+    N = {"explicit": 777.0, "adv_stats": 555.0, "implicit": o_own["stats"]["n_steps"]}[den]
+    o = O_ppo.ppo_loss_chunk(logp, lb, adv, m, np.arange(R) // A, S, n_den=N, **o_kw)
+    if var.get("dual_clip"):
+        assert o["stats"]["n_dual_clipped"] > 0
     g = torch.empty(R, device="cuda")
     lt = torch.empty(R, device="cuda")
     st = torch.zeros(24, dtype=torch.float64, device="cuda")
+    ast = torch.zeros(24, dtype=torch.float64, device="cuda")
+    ast[23] = 555.0
     fa = P.ppo_args(logp_behav=_cuda(lb), adv=_cuda(adv), version=_cuda(ver), slot_key=_cuda(key),
-                    a_tok=A, cur_version=100, ratio_level=1)
+                    a_tok=A, cur_version=100, ratio_level=1,
+                    logp_prox=_cuda(lpp) if prox else None,
+                    tok_denominator=777.0 if den == "explicit" else 0.0,
+                    adv_stats=ast if den == "adv_stats" else None, **kw)
     P.rlvla_ppo_loss(_cuda(logp), _cuda(t), fa, g, lt, st, P.workspace(1))
-    lag = np.repeat(100 - ver.astype(np.int64), A)
-    m = np.repeat(key != 0, A) & (t >= 0) & (lag >= 0) & (lag <= 1)
-    o = O_ppo.ppo_loss_chunk(logp, lb, adv, m, np.arange(R) // A, S)
-    near = np.abs(o["rho_step"] / 1.2 - 1) < 1e-5
-    near |= np.abs(o["rho_step"] / 0.8 - 1) < 1e-5
-    okt = ~np.repeat(near, A)
+    okt = ~np.repeat(o["near_tie_step"], A)
     H.assert_close_rel(g.cpu().numpy()[okt], o["grad"][okt], 1e-5, 1e-9, "chunk grad")
     s = st.cpu().numpy()
     assert abs(s[6] - o["stats"]["loss"]) <= 1e-5 * abs(o["stats"]["loss"]) + 1e-7
-    assert s[18] == o["stats"]["n_steps"] and s[11] == m.sum()
+    assert s[18] == N and s[11] == m.sum()
+    assert s[16] == o["stats"]["n_dual_clipped"] and s[7] == o["stats"]["n_clipped"]
     assert abs(lt.double().sum().item() - o["loss_step"].sum()) <= 1e-4 * abs(o["loss_step"].sum()) + 1e-5
+
+
+def test_ppo_loss_chunk_micro_batches_and_guards():
+    """Streamer micro-batches of the chunk path (accumulate) with N_steps from the stats
+    vector: grads bit-identical to one call, stats within 1e-12; the call's own count with
+    accumulate, or a KL term, are refused; rows = 0 with stats writes zeros."""
+    P = _P()
+    S, A = 300, 56
+    R, logp, lb, lpp, t, adv, ver, key, m = _chunk_case(S, A, seed=5)
+    ast = torch.zeros(24, dtype=torch.float64, device="cuda")
+    ast[23] = 290.0
+    base = dict(logp_behav=_cuda(lb), adv=_cuda(adv), version=_cuda(ver), slot_key=_cuda(key),
+                a_tok=A, cur_version=100, ratio_level=1, adv_stats=ast, logp_prox=_cuda(lpp))
+    g1 = torch.empty(R, device="cuda")
+    st1 = torch.zeros(24, dtype=torch.float64, device="cuda")
+    ws = P.workspace(1)
+    P.rlvla_ppo_loss(_cuda(logp), _cuda(t), P.ppo_args(**base), g1, None, st1, ws)
+    g2 = torch.empty(R, device="cuda")
+    st2 = torch.zeros(24, dtype=torch.float64, device="cuda")
+    lpd, td = _cuda(logp), _cuda(t)
+    for s0, s1 in ((0, 64), (64, 65), (65, 200), (200, 300)):
+        r0, r1 = s0 * A, s1 * A
+        fa = P.ppo_args(logp_behav=base["logp_behav"][r0:r1], adv=base["adv"][s0:s1],
+                        version=base["version"][s0:s1], slot_key=base["slot_key"][s0:s1], a_tok=A,
+                        cur_version=100, ratio_level=1, adv_stats=ast, logp_prox=base["logp_prox"][r0:r1],
+                        accumulate=1)
+        P.rlvla_ppo_loss(lpd[r0:r1], td[r0:r1], fa, g2[r0:r1], None, st2, ws)
+    assert torch.equal(g1, g2)
+    a, b = st1.cpu().numpy(), st2.cpu().numpy()
+    for k in range(6, 19):
+        assert abs(a[k] - b[k]) <= 1e-12 * max(1.0, abs(a[k])), (k, a[k], b[k])
+    o = O_ppo.ppo_loss_chunk(logp, lb, adv, m, np.arange(R) // A, S, n_den=290.0, logp_prox=lpp)
+    assert abs(a[6] - o["stats"]["loss"]) <= 1e-5 * abs(o["stats"]["loss"]) + 1e-7
+    # refused: accumulate without a known N_steps, KL on the chunk path
+    bad = dict(base, adv_stats=None, accumulate=1)
+    with pytest.raises(P.RlvlaError) as e:
+        P.rlvla_ppo_loss(lpd, td, P.ppo_args(**bad), g2, None, st2, ws)
+    assert e.value.status == 1
+    with pytest.raises(P.RlvlaError) as e:
+        P.rlvla_ppo_loss(lpd, td, P.ppo_args(**dict(base, logp_ref=lpd, kl_coef=0.1)), g2, None, st2, ws)
+    assert e.value.status == 2
+    # rows = 0 with stats: this call's totals (zeros), DENOM = N
+    st3 = torch.full((24,), 9.0, dtype=torch.float64, device="cuda")
+    e0 = torch.empty(0, device="cuda")
+    fa0 = P.ppo_args(logp_behav=e0, adv=e0, version=torch.empty(0, dtype=torch.int32, device="cuda"),
+                     slot_key=torch.empty(0, dtype=torch.int64, device="cuda"), a_tok=A,
+                     cur_version=100, ratio_level=1, adv_stats=ast)
+    P.rlvla_ppo_loss(e0, None, fa0, e0, None, st3, ws)
+    s3 = st3.cpu().numpy()
+    assert (s3[6:18] == 0).all() and s3[18] == 290.0 and (s3[:6] == 9.0).all()
 
 
 @pytest.mark.parametrize("clip_eps,denom", [(0.2, 0.0), (0.0, 0.0), (0.5, 1234.0)])

@@ -50,6 +50,7 @@ def _gae_case(T, E, seed, done_p, valid_p):
     ver = (100 - rng.integers(0, 3, size=(E, T))).astype(np.int32)
     tokens = rng.integers(-1, 50, size=(E, T, 3)).astype(np.int32)
     lv = rng.normal(size=E).astype(np.float32)
+    tokens[rng.random((E, T)) < 0.03] = -1       # steps without a usable token (N_LOSS_STEPS)
     return reward, value, done, valid, ver, tokens, lv
 
 
@@ -87,7 +88,7 @@ def test_gae_matches_oracle(T, E, done_p, valid_p, whiten, gamma, lam):
     assert abs(st[1] - s1) <= 1e-5 * max(1.0, np.abs(a).sum())
     assert abs(st[2] - s2) <= 1e-5 * max(1.0, s2)
     c = O_adv.step_counts(valid, ver, tokens, 100, 1)
-    assert (st[3], st[4], st[5]) == (c["n_tok"], c["n_stale"], c["n_bad"])
+    assert (st[3], st[4], st[5], st[23]) == (c["n_tok"], c["n_stale"], c["n_bad"], c["n_loss_steps"])
     if whiten:
         a = O_adv.whiten(a, valid, 1e-8)
     floor = max(1e-3, float(np.sqrt(np.mean(a ** 2))))
@@ -117,6 +118,9 @@ def test_grpo_matches_oracle(E, G, explicit, unbiased):
     prm = P.adv_params("grpo", group_id=torch.from_numpy(gid.astype(np.int32)).cuda() if explicit else None,
                        group_size=G, std_unbiased=unbiased, n_env_global=E, cur_version=100)
     P.rlvla_advantages(buf, None, prm, adv, ret, stats, P.workspace(E))
+    c = O_adv.step_counts(valid, ver, tokens, 100, 1)
+    st = stats.cpu().numpy()
+    assert (st[0], st[3], st[23]) == (c["n_valid"], c["n_tok"], c["n_loss_steps"])
     R = O_adv.episode_return(reward, valid)
     A = O_adv.grpo_step_adv(O_adv.grpo(R, gid, 1e-6, unbiased), valid)
     H.assert_close_rel(adv.cpu().numpy(), A, 1e-5, 1e-3, "grpo adv")
@@ -155,6 +159,8 @@ def test_gae_token_count_multipass():
     reward, value, done, valid, ver, _, lv = _gae_case(300, 512, 11, 0.01, 0.95)
     rng = np.random.default_rng(12)
     tokens = rng.integers(-2, 40, size=(512, 300, 9)).astype(np.int32)
+    tokens[rng.random((512, 300)) < 0.05] = -1             # steps without a usable token
+    tokens[rng.random((512, 300)) < 0.05, :5] = -1         # ... or whose first 5 are ignored
     ver = (100 - rng.integers(-1, 4, size=(512, 300))).astype(np.int32)
     buf = _gpu_buffer(reward, value, done, valid, ver, tokens)
     adv = torch.zeros(512, 300, device="cuda")
@@ -164,6 +170,6 @@ def test_gae_token_count_multipass():
     P.rlvla_advantages(buf, torch.from_numpy(lv).cuda(), prm, adv, ret, stats, P.workspace(512))
     st = stats.cpu().numpy()
     c = O_adv.step_counts(valid, ver, tokens, 100, 1)
-    assert (st[3], st[4], st[5]) == (c["n_tok"], c["n_stale"], c["n_bad"])
+    assert (st[3], st[4], st[5], st[23]) == (c["n_tok"], c["n_stale"], c["n_bad"], c["n_loss_steps"])
     a, _ = O_adv.gae(reward, value, done, valid, lv, 0.99, 0.95)
     H.assert_close_rel(adv.cpu().numpy(), a, 1e-5, max(1e-3, float(np.sqrt(np.mean(a ** 2)))), "adv")

@@ -8,6 +8,15 @@ invariance: the same global problem on one rank vs sharded gives bit-identical G
 and per-row logp / grad / dlogits, and loss statistics within 1e-12.
 
   torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/mgpu_parity.py
+
+RLVLA_MGPU_MODE=p2p-only: no NCCL anywhere — a gloo process group, the library's P2P-only
+communicator (CUDA IPC mailbox handles exchanged over gloo) and ranks placed round-robin on
+the visible GPUs, so 8 ranks run on 4 GPUs (2 per GPU) and the in-kernel C1/C2/C3 exchange
+runs at its full 8-rank capacity.
+
+Also covered: the chunk-ratio path with its default normaliser (the global step count, and
+N_LOSS_STEPS from rlvla_advantages), the value loss with its own global count, and a rank
+whose share of a fused call is empty (it still takes part in C3).
 """
 import os
 import sys
@@ -31,13 +40,46 @@ from tests import harness as H  # noqa: E402
 CUR = synth.CUR_VERSION
 
 
+MODE = os.environ.get("RLVLA_MGPU_MODE", "nccl")
+
+
+def _host_coll(fn, t, *a):
+    """Run a torch collective; with gloo on host copies (results copied back)."""
+    if MODE == "nccl":
+        return fn(t, *a)
+    if isinstance(t, list):
+        h = [x.cpu() for x in t]
+        fn(h, *(x.cpu() for x in a))
+        for x, y in zip(t, h):
+            x.copy_(y)
+        return
+    h = t.cpu()
+    fn(h, *a)
+    t.copy_(h)
+
+
+def all_reduce(t):
+    _host_coll(dist.all_reduce, t)
+
+
+def all_gather(out, t):
+    _host_coll(lambda o, x: dist.all_gather(o, x), out, t)
+
+
 def main():
     world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", rank))
+    ndev = torch.cuda.device_count()
+    local = local % ndev                      # p2p-only: several ranks per GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
-    comm = P.Comm.from_process_group(device=dev)
+    if MODE == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+        comm = P.Comm.from_process_group(device=dev)
+    else:
+        dist.init_process_group("gloo")
+        comm = P.Comm.p2p_from_process_group()
+        assert comm.p2p, "P2P-only communicator did not connect"
     E = 16 * world
     cfg = synth.scaled(synth.CONFIGS["tiny"], n_env=E, group_size=4, interleave_groups=True)
     traj = synth.make_trajectories(cfg)
@@ -78,13 +120,13 @@ def main():
                                              n_env_global=E, cur_version=CUR), adv, ret, st, ws,
                        comm=comm)
     R_all = [torch.zeros(E_r, dtype=torch.float64, device=dev) for _ in range(world)]
-    dist.all_gather(R_all, torch.from_numpy(O_adv.episode_return(obuf["reward"], valid)).to(dev))
+    all_gather(R_all, torch.from_numpy(O_adv.episode_return(obuf["reward"], valid)).to(dev))
     R_glob = torch.cat(R_all).cpu().numpy()
     a_ref = O_adv.grpo_step_adv(O_adv.grpo(R_glob, traj.group_id)[lo:hi], valid)
     H.assert_close_rel(adv.cpu().numpy(), a_ref, 1e-5, 1e-3, "grpo adv (spanning ranks)")
     c = O_adv.step_counts(valid, obuf["version"], obuf["tokens"], CUR, 1)
     tot = torch.tensor([c["n_valid"], c["n_tok"], c["n_stale"], c["n_bad"]], dtype=torch.float64, device=dev)
-    dist.all_reduce(tot)
+    all_reduce(tot)
     s = st.cpu().numpy()
     assert (s[0], s[3], s[4], s[5]) == tuple(tot.cpu().numpy().tolist()), (s[:6], tot)
     # GAE + global whitening (C1)
@@ -94,7 +136,7 @@ def main():
                                              cur_version=CUR), adv2, ret, st2, ws, comm=comm)
     a_gae, _ = O_adv.gae(obuf["reward"], obuf["value"], obuf["done"], valid, traj.last_value[lo:hi], 0.99, 0.95)
     ws_ = torch.tensor(O_adv.whiten_stats(a_gae, valid), dtype=torch.float64, device=dev)
-    dist.all_reduce(ws_)
+    all_reduce(ws_)
     a_w = O_adv.whiten(a_gae, valid, 1e-8, stats=tuple(ws_.cpu().numpy()))
     H.assert_close_rel(adv2.cpu().numpy(), a_w, 1e-5, max(1e-3, float(np.sqrt(np.mean(a_w ** 2)))), "gae whitened")
     # fused loss with global N_tok (from st) and C3
@@ -117,7 +159,7 @@ def main():
     H.assert_close_rel(g.cpu().numpy()[~nt], ref["ppo"]["grad"][~nt], 1e-5, 1e-7, "grad (global N)")
     rs = torch.tensor([ref["stats"][k] for k in ("loss", "n_loss_tok", "entropy_sum")],
                       dtype=torch.float64, device=dev)
-    dist.all_reduce(rs)
+    all_reduce(rs)
     s3 = st3.cpu().numpy()
     rs = rs.cpu().numpy()
     assert abs(s3[6] - rs[0]) <= 1e-5 * max(1e-3, abs(rs[0])), (s3[6], rs[0])
@@ -177,7 +219,7 @@ def main():
     o = O_ppo.value_loss(v, vo, Rt, key != 0, clip_eps=0.2, n_den=Nv)
     H.assert_close_rel(gv.cpu().numpy(), o["grad"], 1e-5, 1e-9, "value grad")
     rv = torch.tensor([o["stats"]["loss"], float((key != 0).sum())], dtype=torch.float64, device=dev)
-    dist.all_reduce(rv)
+    all_reduce(rv)
     s4 = st4.cpu().numpy()
     assert abs(s4[19] - rv[0].item()) <= 1e-5 * abs(rv[0].item()) and s4[21] == rv[1].item()
     # NEXT-4 flow chain + PPO: one ratio per step, C3 over the ranks
@@ -201,7 +243,7 @@ def main():
     ok = ~pf["near_tie"]
     H.assert_close_rel(gf.cpu().numpy()[ok], pf["grad"][ok], 1e-4, 1e-6, "flow grad")
     rf = torch.tensor([pf["stats"]["loss"], float(Rf)], dtype=torch.float64, device=dev)
-    dist.all_reduce(rf)
+    all_reduce(rf)
     s5 = st5.cpu().numpy()
     assert abs(s5[6] - rf[0].item()) <= 1e-4 * max(1e-3, abs(rf[0].item())), (s5[6], rf[0].item())
     assert s5[11] == rf[1].item() and s5[18] == Nf
@@ -220,12 +262,68 @@ def main():
     oc = O_ppo.ppo_loss_chunk(lpc, lbc, advc, np.ones(Rc, bool), np.arange(Rc) // A2, S, n_den=1000.0)
     H.assert_close_rel(gc.cpu().numpy(), oc["grad"], 1e-4, 1e-9, "chunk grad")
     rc = torch.tensor([oc["stats"]["loss"]], dtype=torch.float64, device=dev)
-    dist.all_reduce(rc)
+    all_reduce(rc)
     s6 = st6.cpu().numpy()
     assert abs(s6[6] - rc[0].item()) <= 1e-4 * max(1e-3, abs(rc[0].item())), (s6[6], rc[0].item())
+    # NEXT-2 chunk ratio with its DEFAULT normaliser: the call's own masked steps over all
+    # ranks (it was this rank's count only), then N_LOSS_STEPS of rlvla_advantages
+    tc = np.where(rng.random(Rc) < 0.05, -1, 3).astype(np.int32)
+    tc[:A2] = -1                                                      # a step without tokens
+    gc2 = torch.empty(Rc, device=dev)
+    st7 = torch.zeros(24, dtype=torch.float64, device=dev)
+    fa = P.ppo_args(logp_behav=cu(lbc), adv=cu(advc), version=cu(np.full(S, CUR, np.int32)),
+                    slot_key=cu(np.ones(S, np.int64)), a_tok=A2, cur_version=CUR, ratio_level=1)
+    P.rlvla_ppo_loss(cu(lpc), cu(tc), fa, gc2, None, st7, ws, comm=comm)
+    mc = tc >= 0
+    n_loc = O_ppo.ppo_loss_chunk(lpc, lbc, advc, mc, np.arange(Rc) // A2, S)["stats"]["n_steps"]
+    ng = torch.tensor([n_loc], dtype=torch.float64, device=dev)
+    all_reduce(ng)
+    Ng = float(ng.item())
+    oc2 = O_ppo.ppo_loss_chunk(lpc, lbc, advc, mc, np.arange(Rc) // A2, S, n_den=Ng)
+    H.assert_close_rel(gc2.cpu().numpy(), oc2["grad"], 1e-4, 1e-9, "chunk grad (global own count)")
+    rc2 = torch.tensor([oc2["stats"]["loss"]], dtype=torch.float64, device=dev)
+    all_reduce(rc2)
+    s7 = st7.cpu().numpy()
+    assert s7[18] == Ng, (s7[18], Ng)
+    assert abs(s7[6] - rc2.item()) <= 1e-4 * max(1e-3, abs(rc2.item())), (s7[6], rc2.item())
+    # ... and N_steps = N_LOSS_STEPS of the buffer's advantages call (global over ranks)
+    c_all = torch.tensor([c["n_loss_steps"]], dtype=torch.float64, device=dev)
+    all_reduce(c_all)
+    assert st[23].item() == c_all.item(), (st[23].item(), c_all.item())
+    # NEXT-2 value loss with its own count over all ranks (no explicit N_v)
+    gv2 = torch.empty(nv, device=dev)
+    st8 = torch.zeros(24, dtype=torch.float64, device=dev)
+    P.rlvla_value_loss(cu(v), cu(vo), cu(Rt), cu(key), cu(ver), CUR, gv2, clip_eps=0.2,
+                       stats=st8, ws=ws, comm=comm)
+    Nv2 = torch.tensor([float((key != 0).sum())], dtype=torch.float64, device=dev)
+    all_reduce(Nv2)
+    o2 = O_ppo.value_loss(v, vo, Rt, key != 0, clip_eps=0.2, n_den=float(Nv2.item()))
+    H.assert_close_rel(gv2.cpu().numpy(), o2["grad"], 1e-5, 1e-9, "value grad (global own count)")
+    rv2 = torch.tensor([o2["stats"]["loss"]], dtype=torch.float64, device=dev)
+    all_reduce(rv2)
+    s8 = st8.cpu().numpy()
+    assert s8[22] == Nv2.item() and abs(s8[19] - rv2.item()) <= 1e-5 * abs(rv2.item())
+    # a rank with NO rows in a fused call still takes part in C3: rank 0 empty
+    xs = xr if rank != 0 else xr[:0]
+    n_ = xs.shape[0]
+    so = torch.zeros(24, dtype=torch.float64, device=dev)
+    fa_ = P.ppo_args(logp_behav=buf.logp_behav.view(-1)[:n_], adv=adv.view(-1), version=buf.version.view(-1),
+                     slot_key=buf.slot_key.view(-1), a_tok=A, cur_version=CUR, adv_stats=st,
+                     out_grad_logp=torch.empty(n_, device=dev))
+    P.rlvla_logprob_fwd_bwd(xs, buf.tokens.view(-1)[:n_], logp=torch.empty(n_, device=dev), fused=fa_,
+                            dlogits=torch.empty_like(xs), stats=so, ws=ws, comm=comm)
+    tv0 = O_path.token_view(obuf, a_ref.astype(np.float32).astype(np.float64), A, CUR)
+    mine = O_path.loss_and_grad(x[lo * T * A:hi * T * A], tv0, n_tok=float(tot[1].item()))["stats"]
+    re = torch.tensor([0.0 if rank == 0 else mine["loss"], 0.0 if rank == 0 else mine["n_loss_tok"]],
+                      dtype=torch.float64, device=dev)
+    all_reduce(re)
+    so_ = so.cpu().numpy()
+    assert abs(so_[6] - re[0].item()) <= 1e-5 * max(1e-3, abs(re[0].item())), (so_[6], re[0].item())
+    assert so_[11] == re[1].item()
     dist.barrier()
     if rank == 0:
-        print(f"MGPU PARITY OK world={world} nccl={P.rlvla_nccl_version()} "
+        nccl = P.rlvla_nccl_version() if MODE == "nccl" else "none"
+        print(f"MGPU PARITY OK world={world} mode={MODE} gpus={ndev} nccl={nccl} "
               f"in-kernel-p2p={comm.p2p}", flush=True)
     comm.destroy()
     dist.destroy_process_group()
