@@ -46,6 +46,11 @@ def parse():
                     help="logit rows per fused call (Streamer micro-batch, P:88); 0 = all rows "
                          "if they fit, else ~131072 rows of whole envs")
     ap.add_argument("--chunk", type=int, default=synth.B_MAX)
+    ap.add_argument("--schedule", default="pipelined", choices=["pipelined", "serial"],
+                    help="pipelined: S1+S2 of batch i+1 on a rollout-side stream while S3+S4 of "
+                         "batch i runs (double-buffered trajectory buffer); serial: one stream")
+    ap.add_argument("--reserve-sms", type=int, default=1,
+                    help="pipelined: SMs the persistent log-prob kernel leaves to the other stream")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--eager", action="store_true",
@@ -214,29 +219,40 @@ def run_ours(args):
     drec = P.StepBatch(**{k: v.to(dev) for k, v in host.items()})
     h2d_bytes = sum(v.numel() * v.element_size() for v in host.values())
 
-    buf = P.TrajectoryBuffer.allocate(E_r, T, A, device=dev)
-    counters = torch.zeros(4, dtype=torch.int64, device=dev)
-    adv = torch.zeros(E_r, T, device=dev)
-    ret = torch.zeros(E_r, T, device=dev)
-    stats = torch.zeros(24, dtype=torch.float64, device=dev)
+    # two trajectory buffers (with their advantages / statistics): in the pipelined schedule
+    # batch i+1 streams into one (S1) and gets its advantages (S2) on the rollout-side stream
+    # while the actor's S3+S4 reads batch i from the other (§3.1 rollout keeps running on
+    # the pre-update policy; §3.3 the Streamer masks data preparation time)
+    # (the pipelined schedule needs the in-kernel exchanges when N > 1: two streams must not
+    # interleave NCCL collectives of one communicator)
+    nbuf = 2 if args.schedule == "pipelined" and (comm is None or comm.p2p) else 1
+    bufs = [P.TrajectoryBuffer.allocate(E_r, T, A, device=dev) for _ in range(nbuf)]
+    cnts = [torch.zeros(4, dtype=torch.int64, device=dev) for _ in range(nbuf)]
+    advs = [torch.zeros(E_r, T, device=dev) for _ in range(nbuf)]
+    rets = [torch.zeros(E_r, T, device=dev) for _ in range(nbuf)]
+    statss = [torch.zeros(24, dtype=torch.float64, device=dev) for _ in range(nbuf)]
+    wss = [P.workspace(E, device=dev) for _ in range(nbuf)]   # S2 (rollout-side stream)
+    ws_act = P.workspace(E, device=dev)                       # S3+S4 (actor stream)
     lstats = torch.zeros(24, dtype=torch.float64, device=dev)
     logp = torch.empty(R, device=dev)
-    ws = P.workspace(E, device=dev)
     lv = torch.from_numpy(traj.last_value[lo:hi]).to(dev)
     gid = torch.from_numpy(traj.group_id).to(dev)
     prm = P.adv_params(cfg.adv_mode, whiten=cfg.whiten,
                        group_id=gid if cfg.adv_mode == "grpo" else None,
                        group_size=cfg.group_size, env_offset=lo, n_env_global=E,
                        cur_version=synth.CUR_VERSION, max_staleness=1)
-    fas = []
-    for i, (m0, m1) in enumerate(mbs):
-        s0, s1 = m0 // A, m1 // A
-        fas.append(P.ppo_args(logp_behav=buf.logp_behav.view(-1)[m0:m1], adv=adv.view(-1)[s0:s1],
-                              version=buf.version.view(-1)[s0:s1],
-                              slot_key=buf.slot_key.view(-1)[s0:s1], a_tok=A,
-                              cur_version=synth.CUR_VERSION, max_staleness=1, adv_stats=stats,
-                              accumulate=i > 0))
-    tgt_flat = buf.tokens.view(-1)
+    fass = []
+    for k in range(nbuf):
+        b, a_, st_ = bufs[k], advs[k], statss[k]
+        fas = []
+        for i, (m0, m1) in enumerate(mbs):
+            s0, s1 = m0 // A, m1 // A
+            fas.append(P.ppo_args(logp_behav=b.logp_behav.view(-1)[m0:m1], adv=a_.view(-1)[s0:s1],
+                                  version=b.version.view(-1)[s0:s1],
+                                  slot_key=b.slot_key.view(-1)[s0:s1], a_tok=A,
+                                  cur_version=synth.CUR_VERSION, max_staleness=1, adv_stats=st_,
+                                  accumulate=i > 0))
+        fass.append(fas)
     chunks = synth.arrival_chunks(rec.n, args.chunk)
     chunk_batches = [drec.slice(sl) for sl in chunks]
     nmb = len(mbs)
@@ -247,32 +263,76 @@ def run_ours(args):
     # per-stage events (S1/S2 are latency-bound, reported in us per call)
     ev_sa = [cr.event() for _ in range(args.steps)]   # before the scatter calls
     ev_sb = [cr.event() for _ in range(args.steps)]   # after the scatter calls
+    ev_ad = [cr.event() for _ in range(args.steps)]   # before rlvla_advantages
     ev_sc = [cr.event() for _ in range(args.steps)]   # after rlvla_advantages
+    s_roll = torch.cuda.Stream(device=dev) if nbuf == 2 else None
+    if nbuf == 2:
+        P.rlvla_set_reserved_sms(args.reserve_sms)
+    st_pinned = torch.empty(lstats.numel(), dtype=torch.float64).pin_memory()
+    dst = {k: getattr(drec, k) for k in host}
 
-    def step(i=None, capturing=False):
-        stream = torch.cuda.current_stream()
+    def prepare(i, k, stream, timed, capturing, e2e):
+        """S1 + S2 of batch i into buffer k on `stream` (records H2D first for e2e)."""
         sh = stream.cuda_stream
-        buf.reset()
-        counters.zero_()
-        seq = 1
-        if i is not None:
-            cr.record(ev_sa[i], sh, capturing)
-        for sl, cb in zip(chunks, chunk_batches):
-            P.rlvla_scatter_steps(buf, cb, synth.CUR_VERSION, seq, counters, stream=stream)
-            seq += sl.stop - sl.start
-        if i is not None:
-            cr.record(ev_sb[i], sh, capturing)
-        P.rlvla_advantages(buf, lv, prm, adv, ret, stats, ws, comm=comm, stream=stream)
-        if i is not None:
-            cr.record(ev_sc[i], sh, capturing)
-        for j, ((m0, m1), fa) in enumerate(zip(mbs, fas)):
-            if i is not None:
+        with torch.cuda.stream(stream):
+            if e2e:
+                for key, v in host.items():
+                    dst[key].copy_(v, non_blocking=True)
+            bufs[k].reset()
+            cnts[k].zero_()
+            if timed:
+                cr.record(ev_sa[i], sh, capturing)
+            seq = 1
+            for sl, cb in zip(chunks, chunk_batches):
+                P.rlvla_scatter_steps(bufs[k], cb, synth.CUR_VERSION, seq, cnts[k], stream=stream)
+                seq += sl.stop - sl.start
+            if timed:
+                cr.record(ev_sb[i], sh, capturing)
+                cr.record(ev_ad[i], sh, capturing)
+            P.rlvla_advantages(bufs[k], lv, prm, advs[k], rets[k], statss[k], wss[k], comm=comm,
+                               stream=stream)
+            if timed:
+                cr.record(ev_sc[i], sh, capturing)
+
+    def actor(i, k, stream, timed, capturing, e2e):
+        """S3 + S4 (fused log-prob + PPO fwd/bwd, dlogits, loss statistics) on buffer k."""
+        sh = stream.cuda_stream
+        for j, ((m0, m1), fa) in enumerate(zip(mbs, fass[k])):
+            if timed:
                 cr.record(ev_k0[i * nmb + j], sh, capturing)
-            P.rlvla_logprob_fwd_bwd(logits[:m1 - m0], tgt_flat[m0:m1], logp=logp[m0:m1], fused=fa,
-                                    dlogits=dlogits[:m1 - m0], stats=lstats, ws=ws,
+            P.rlvla_logprob_fwd_bwd(logits[:m1 - m0], bufs[k].tokens.view(-1)[m0:m1], logp=logp[m0:m1],
+                                    fused=fa, dlogits=dlogits[:m1 - m0], stats=lstats, ws=ws_act,
                                     comm=comm if j == nmb - 1 else None, stream=stream)
-            if i is not None:
+            if timed:
                 cr.record(ev_k1[i * nmb + j], sh, capturing)
+        if e2e:
+            st_pinned.copy_(lstats, non_blocking=True)
+
+    def run_steps(n, timed=False, capturing=False, e2e=False):
+        """n whole steps (batches). serial: S1, S2, S3+S4 of batch i back to back on one
+        stream. pipelined: S1+S2 of batch i+1 on the rollout-side stream while the actor's
+        S3+S4 of batch i runs (double-buffered); the first batch's preparation is exposed."""
+        main = torch.cuda.current_stream()
+        if nbuf == 1:
+            for i in range(n):
+                prepare(i, 0, main, timed, capturing, e2e)
+                actor(i, 0, main, timed, capturing, e2e)
+            return
+        ready = [torch.cuda.Event() for _ in range(n)]
+        done = [torch.cuda.Event() for _ in range(n)]
+        s_roll.wait_stream(main)                               # fork
+        prepare(0, 0, s_roll, timed, capturing, e2e)
+        ready[0].record(s_roll)
+        for i in range(n):
+            if i + 1 < n:
+                if i >= 1:                   # buffer (i+1) % 2 was read by batch i-1's actor
+                    s_roll.wait_event(done[i - 1])
+                prepare(i + 1, (i + 1) % 2, s_roll, timed, capturing, e2e)
+                ready[i + 1].record(s_roll)
+            main.wait_event(ready[i])
+            actor(i, i % 2, main, timed, capturing, e2e)
+            done[i].record(main)
+        main.wait_stream(s_roll)                               # join
 
     n_adv_kernels = 2 if (cfg.adv_mode == "grpo" or cfg.whiten) else 1
     launches_per_step = len(chunks) + n_adv_kernels + nmb   # scatter chunks + advantages + fused
@@ -281,19 +341,17 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
-    for _ in range(args.warmup):
-        step()
+    run_steps(args.warmup)
     torch.cuda.synchronize()
     graph = None
     if not args.eager:
-        # the K timed steps as ONE captured graph (event nodes around every fused launch)
+        # the K timed steps as ONE captured graph (event nodes around every stage)
         try:
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph):
                 cs = torch.cuda.current_stream().cuda_stream
                 cr.record(ev_t0, cs, True)
-                for i in range(args.steps):
-                    step(i, capturing=True)
+                run_steps(args.steps, timed=True, capturing=True)
                 cr.record(ev_t1, cs, True)
             graph.replay()                      # one untimed replay (graph upload / warm-up)
             torch.cuda.synchronize()
@@ -310,8 +368,7 @@ def run_ours(args):
         graph.replay()
     else:
         cr.record(ev_t0, stream.cuda_stream, False)
-        for i in range(args.steps):
-            step(i)
+        run_steps(args.steps, timed=True)
         cr.record(ev_t1, stream.cuda_stream, False)
     torch.cuda.synchronize()
     barrier()
@@ -319,17 +376,17 @@ def run_ours(args):
     ms = cr.elapsed(ev_t0, ev_t1)
     k_ms = [cr.elapsed(a, b) for a, b in zip(ev_k0, ev_k1)]   # one per fused launch
     sc_ms = sorted(cr.elapsed(a, b) for a, b in zip(ev_sa, ev_sb))
-    ad_ms = sorted(cr.elapsed(a, b) for a, b in zip(ev_sb, ev_sc))
+    ad_ms = sorted(cr.elapsed(a, b) for a, b in zip(ev_ad, ev_sc))
     if args.trace and rank == 0:
         # chrome://tracing / Perfetto: one complete event per stage of every timed step,
         # timestamps relative to the start of the timed region (CUDA events, microseconds)
         evs = []
         for i in range(args.steps):
             t_s = cr.elapsed(ev_t0, ev_sa[i]) * 1e3
-            evs.append(dict(name="S1 scatter (64 chunks)", ph="X", pid=0, tid=0, ts=t_s,
+            evs.append(dict(name="S1 scatter (64 chunks)", ph="X", pid=0, tid=1 if nbuf == 2 else 0, ts=t_s,
                             dur=cr.elapsed(ev_sa[i], ev_sb[i]) * 1e3))
-            evs.append(dict(name="S2 advantages", ph="X", pid=0, tid=0, ts=cr.elapsed(ev_t0, ev_sb[i]) * 1e3,
-                            dur=cr.elapsed(ev_sb[i], ev_sc[i]) * 1e3))
+            evs.append(dict(name="S2 advantages", ph="X", pid=0, tid=1 if nbuf == 2 else 0, ts=cr.elapsed(ev_t0, ev_ad[i]) * 1e3,
+                            dur=cr.elapsed(ev_ad[i], ev_sc[i]) * 1e3))
             for j in range(nmb):
                 a_, b_ = ev_k0[i * nmb + j], ev_k1[i * nmb + j]
                 evs.append(dict(name=f"S3+S4 fused (micro-batch {j})", ph="X", pid=0, tid=0,
@@ -337,29 +394,18 @@ def run_ours(args):
         with open(args.trace, "w") as f:
             json.dump({"traceEvents": evs, "displayTimeUnit": "ms"}, f)
     st_host = lstats.cpu().numpy()
-    cnt = counters.cpu().numpy()
+    cnt = cnts[(args.steps - 1) % nbuf].cpu().numpy()
 
     # ---- e2e: records from pinned host memory, stats back to host, every step -------
     e2e_ms = None
     if not args.no_e2e:
-        st_pinned = torch.empty(lstats.numel(), dtype=torch.float64).pin_memory()
-        dst = {k: getattr(drec, k) for k in host}
-
-        def e2e_step():
-            for k, v in host.items():
-                dst[k].copy_(v, non_blocking=True)
-            step()
-            st_pinned.copy_(lstats, non_blocking=True)
-
-        for _ in range(min(2, args.warmup)):
-            e2e_step()
+        run_steps(min(2, args.warmup), e2e=True)
         torch.cuda.synchronize()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         stream = torch.cuda.current_stream()
         e0.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
+        run_steps(args.steps, e2e=True)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -400,6 +446,9 @@ def run_ours(args):
                    "rows_per_gpu": R, "records_per_gpu": rec.n, "arrival_chunk": args.chunk,
                    "fused_calls_per_step": nmb, "rows_per_fused_call": MB,
                    "launch": "one CUDA graph of the K timed steps" if graph is not None else "eager",
+                   "schedule": ("pipelined: S1+S2 of batch i+1 on a second stream during S3+S4 "
+                                f"of batch i (double-buffered trajectory buffer, {args.reserve_sms} SM "
+                                "left free by the persistent kernel)") if nbuf == 2 else "serial",
                    "advantages": cfg.adv_mode, "group_size": cfg.group_size,
                    "groups_span_ranks": bool(groups_span),
                    "l2": f"inputs larger than L2: {R * V * 2 / 1e9:.1f} GB logits read + same "

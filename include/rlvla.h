@@ -443,6 +443,14 @@ RLVLA_API rlvla_status rlvla_comm_connect_p2p(rlvla_comm c, const void* all_hand
  * value loss reduces slots 19..21 and the chunk-ratio path slots 6..17 the same way. */
 RLVLA_API int32_t rlvla_comm_p2p_enabled(rlvla_comm c);
 
+/* Launch policy (host, process-wide, thread-safe): the persistent kernels (TMA log-prob
+ * kernel, TMA flow kernel: one CTA per SM holding the register file) use sm_count - n SMs
+ * (at least 1), leaving n SMs free so latency-bound work on another stream (e.g. the next
+ * batch's rlvla_scatter_steps / rlvla_advantages while the actor's S3+S4 runs: §3.3
+ * "masking data preparation time") is not blocked until they finish. Default 0. Returns
+ * the previous value. */
+RLVLA_API int32_t rlvla_set_reserved_sms(int32_t n);
+
 RLVLA_API const char* rlvla_status_string(rlvla_status s);
 RLVLA_API int32_t rlvla_abi_version(void);
 /* Version of the NCCL library actually loaded (e.g. 22809), 0 if unavailable. */

@@ -9,6 +9,7 @@ from .api import (  # noqa: F401
     ppo_args, rlvla_abi_version, rlvla_advantages, rlvla_batch_offer, rlvla_batch_poll,
     rlvla_flow_logprob,
     rlvla_logprob_fwd_bwd, rlvla_nccl_version, rlvla_ppo_loss, rlvla_scatter_steps,
+    rlvla_set_reserved_sms,
     rlvla_value_loss, rlvla_workspace_bytes, workspace)
 from . import _abi as abi  # noqa: F401
 from . import sharding  # noqa: F401

@@ -107,6 +107,7 @@ _SIGS = {
     "rlvla_comm_connect_p2p": (c_int32, [c_void_p, c_void_p]),
     "rlvla_status_string": (ctypes.c_char_p, [c_int32]),
     "rlvla_abi_version": (c_int32, []),
+    "rlvla_set_reserved_sms": (c_int32, [c_int32]),
     "rlvla_nccl_version": (c_int32, []),
 }
 

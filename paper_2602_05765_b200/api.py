@@ -300,6 +300,11 @@ def rlvla_workspace_bytes(rows: int, n_env_global: int, t_steps: int) -> int:
     return int(lib().rlvla_workspace_bytes(rows, n_env_global, t_steps))
 
 
+def rlvla_set_reserved_sms(n: int) -> int:
+    """SMs the persistent kernels leave free for other streams; returns the previous value."""
+    return int(lib().rlvla_set_reserved_sms(int(n)))
+
+
 def rlvla_abi_version() -> int:
     return int(lib().rlvla_abi_version())
 

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <vector>
 #include <mutex>
+#include <atomic>
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -52,6 +53,14 @@ const DeviceInfo& device_info() {
     d.device = dev;
   }
   return d;
+}
+
+namespace {
+std::atomic<int> g_reserved_sms{0};
+}
+int persistent_sms() {
+  const int n = device_info().sm_count - g_reserved_sms.load(std::memory_order_relaxed);
+  return n < 1 ? 1 : n;
 }
 
 bool sync_check_enabled() {
@@ -172,6 +181,11 @@ rlvla_status stats_only_call(const rlvla_ppo_args& f, double* stats, void* works
 extern "C" {
 
 RLVLA_API int32_t rlvla_abi_version(void) { return RLVLA_ABI_VERSION; }
+
+RLVLA_API int32_t rlvla_set_reserved_sms(int32_t n) {
+  if (n < 0) n = 0;
+  return g_reserved_sms.exchange(n);
+}
 
 RLVLA_API const char* rlvla_status_string(rlvla_status s) {
   switch (s) {

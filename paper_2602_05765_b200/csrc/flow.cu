@@ -678,7 +678,7 @@ cudaError_t launch_tma(const FlowArgs& a, cudaStream_t s) {
   if (per_sm < 1) per_sm = 1;
   const int64_t tiles = (a.c.rows + kTile - 1) / kTile;
   int64_t grid = (tiles + kTmaWarps - 1) / kTmaWarps;
-  const int64_t cap = int64_t(device_info().sm_count) * per_sm;
+  const int64_t cap = int64_t(persistent_sms()) * per_sm;
   if (grid > cap) grid = cap;
   flow_tma_kernel<T, MODE, NQ, LEARNED, WARPS, STAGES><<<int(grid), kTmaWarps * 32, smem, s>>>(a);
   return cudaGetLastError();

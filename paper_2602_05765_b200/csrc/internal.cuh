@@ -321,6 +321,9 @@ struct DeviceInfo {
   int smem_optin = 0;
 };
 const DeviceInfo& device_info();          // cached per device (thread-safe)
+// SMs the persistent (grid-stride, one-CTA-per-SM) kernels leave free for concurrent work on
+// other streams (rlvla_set_reserved_sms); their grid is sm_count - reserved (>= 1)
+int persistent_sms();
 bool sync_check_enabled();
 
 // launches (return cudaError_t of the launch)

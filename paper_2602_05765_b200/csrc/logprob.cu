@@ -893,7 +893,8 @@ cudaError_t launch_mode(const LpArgs& a, Lp p, cudaStream_t s) {
       if (e != cudaSuccess) return e;
       cached = int(smem);
     }
-    int grid = int(R < sms ? R : sms);
+    const int psms = persistent_sms();
+    int grid = int(R < psms ? R : psms);
     if (xp) {
       if (f7) lp_tma_kernel<MODE, true, 7><<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);
       else lp_tma_kernel<MODE, true, 0><<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);

@@ -17,7 +17,7 @@ def L():
 
 def test_exports_every_header_symbol(L):
     names = A.header_functions()
-    assert len(names) == 18
+    assert len(names) == 19
     for n in names:
         assert hasattr(L, n), n
     assert set(names) == set(A._SIGS)
@@ -25,6 +25,7 @@ def test_exports_every_header_symbol(L):
 
 def test_host_only_calls(L):
     assert L.rlvla_abi_version() == 2
+    assert L.rlvla_set_reserved_sms(2) == 0 and L.rlvla_set_reserved_sms(0) == 2
     assert L.rlvla_nccl_version() >= 22800
     for s in range(6):
         assert L.rlvla_status_string(s)

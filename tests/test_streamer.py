@@ -68,3 +68,93 @@ def test_streamer_equals_full_batch(cfg_name, n_env):
             tot[k] = tot.get(k, 0.0) + v
     assert abs(b[6] - tot["loss"]) <= 1e-5 * max(1e-3, abs(tot["loss"]))
     assert b[11] == tot["n_loss_tok"]
+
+
+def _sub_buffer(P, buf, e0, e1):
+    """Envs [e0, e1) of a trajectory buffer as a buffer of its own (views, no copy)."""
+    return P.TrajectoryBuffer(e1 - e0, buf.t_steps, buf.a_tok, *(getattr(buf, f)[e0:e1] for f in (
+        "slot_key", "reward", "done", "value", "version", "tokens", "logp_behav")))
+
+
+@pytest.mark.parametrize("reserve", [0, 1])
+def test_streamer_interleaved_two_streams(reserve):
+    """The Streamer schedule (P:88 §3.3) on two streams: micro-batch k = whole GRPO groups;
+    its records are scattered and its advantages computed on a rollout-side stream while the
+    actor stream runs the fused S3+S4 of micro-batch k-1 (explicit global denominator,
+    statistics accumulated in micro-batch order; the persistent kernel leaves `reserve` SMs
+    free). Buffer, advantages, logp, grad and dlogits are bit-identical to the serial
+    full-batch path, statistics within 1e-12."""
+    import paper_2602_05765_b200 as P
+    G = 2
+    cfg = synth.scaled(synth.CONFIGS["libero_spatial_oft"], n_env=6, group_size=G)
+    case = H.build_case(cfg, device="cuda")
+    A, T = cfg.a_tok, cfg.t_steps
+    E = cfg.n_env
+    x = case.logits.cuda()
+    R = x.shape[0]
+    obuf, _ = H.oracle_scatter(case)
+    N = float(H.oracle_advantages(case, obuf, "grpo")["counts"]["n_tok"])
+    # serial reference: whole batch on one stream
+    buf_s, _ = H.gpu_scatter(case)
+    adv_s = torch.zeros(E, T, device="cuda")
+    P.rlvla_advantages(buf_s, None, P.adv_params("grpo", group_size=G, n_env_global=E, cur_version=synth.CUR_VERSION),
+                       adv_s, torch.zeros(E, T, device="cuda"), torch.zeros(24, dtype=torch.float64, device="cuda"),
+                       P.workspace(E))
+    st_s = torch.zeros(24, dtype=torch.float64, device="cuda")
+    ref = _fused(P, x, buf_s.tokens.view(-1), buf_s, adv_s, (0, R), A, N, st_s, P.workspace(E), False)
+    # streamer: micro-batch k = group k (envs [kG, kG + G)), its records in arrival order
+    rec = H.to_dev_batch(case)
+    env_np = case.rec.env_id
+    buf = P.TrajectoryBuffer.allocate(E, T, A)
+    adv = torch.zeros(E, T, device="cuda")
+    st = torch.zeros(24, dtype=torch.float64, device="cuda")
+    ws_roll, ws_act = P.workspace(G), P.workspace(E)
+    side = torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    prev = P.rlvla_set_reserved_sms(reserve)
+    outs, seq = [], 1
+    nmb = E // G
+    mbs, idxs = [], []
+    for k in range(nmb):          # each micro-batch's records (local env ids), built up front
+        e0 = k * G
+        idx = np.nonzero((env_np >= e0) & (env_np < e0 + G))[0]
+        it = torch.from_numpy(idx).cuda()
+        mb = P.StepBatch(*(getattr(rec, f)[it].contiguous() for f in (
+            "env_id", "step", "version", "reward", "done", "value", "tokens", "logp_behav")))
+        mb.env_id.sub_(e0)
+        mbs.append(mb)
+        idxs.append(idx)
+    try:
+        side.wait_stream(main)
+        ready = [torch.cuda.Event() for _ in range(nmb)]
+        for k in range(nmb):
+            e0, e1 = k * G, (k + 1) * G
+            sub = _sub_buffer(P, buf, e0, e1)
+            idx, mb = idxs[k], mbs[k]
+            with torch.cuda.stream(side):
+                cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+                for c0 in range(0, len(idx), synth.B_MAX):
+                    c1 = min(len(idx), c0 + synth.B_MAX)
+                    P.rlvla_scatter_steps(sub, mb.slice(slice(c0, c1)), synth.CUR_VERSION, seq + c0, cnt,
+                                          stream=side)
+                P.rlvla_advantages(sub, None, P.adv_params("grpo", group_size=G, n_env_global=G,
+                                                           cur_version=synth.CUR_VERSION),
+                                   adv[e0:e1], torch.zeros(G, T, device="cuda"),
+                                   torch.zeros(24, dtype=torch.float64, device="cuda"), ws_roll, stream=side)
+                ready[k].record(side)
+            seq += len(idx)
+            main.wait_event(ready[k])
+            outs.append(_fused(P, x, buf.tokens.view(-1), buf, adv, (e0 * T * A, e1 * T * A), A, N, st,
+                               ws_act, k > 0))
+        torch.cuda.synchronize()
+    finally:
+        P.rlvla_set_reserved_sms(prev)
+    gb, gs = H.buf_to_np(buf), H.buf_to_np(buf_s)
+    for k in gb:
+        assert np.array_equal(gb[k].view(np.uint8), gs[k].view(np.uint8)) or k == "slot_key", k
+    assert np.array_equal(gb["slot_key"] != 0, gs["slot_key"] != 0)
+    assert torch.equal(adv, adv_s)
+    for j in range(3):
+        assert torch.equal(torch.cat([o[j] for o in outs]), ref[j]), j
+    a, b = st_s.cpu().numpy(), st.cpu().numpy()
+    np.testing.assert_allclose(b[6:18], a[6:18], rtol=1e-12, atol=1e-15)
