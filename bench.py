@@ -504,11 +504,27 @@ def run_ours(args):
 # --------------------------------------------------------------------------------------
 # oracle timing (cpu_baseline leg and --impl reference)
 # --------------------------------------------------------------------------------------
-def oracle_sample_step(cfg, traj, logits_rows_fn, n_env_sample):
-    """The oracle's whole path over `n_env_sample` envs of the workload (their records in
-    arrival order, their logit rows). Returns seconds."""
+_ORACLE_X = None      # fork-shared logits of the all-cores oracle leg (set before the fork)
+
+
+def _oracle_rows(job):
+    """One worker's share of the oracle's S3+S4 (rows are independent): the loss
+    statistics of rows [r0, r1) (dlogits computed, not shipped back)."""
     from oracle import path as O_path
+    r0, r1, n_tok, tv = job
+    out = O_path.loss_and_grad(_ORACLE_X[r0:r1], tv, n_tok=n_tok, rows=np.arange(r0, r1))
+    return out["stats"]
+
+
+def oracle_sample_step(cfg, traj, logits_rows_fn, n_env_sample, pool=None, nproc=1):
+    """The oracle's whole path over `n_env_sample` envs of the workload (their records in
+    arrival order, their logit rows), stage by stage as oracle.path.rollout_to_loss composes
+    it: S1 scatter of every arrival chunk, S2 advantages, S3+S4 loss and dlogits. With a
+    process pool, S3+S4 is split into `nproc` row blocks whose statistics are combined in
+    block order (S1/S2 stay serial: they are < 1 % of the work). Returns per-stage seconds."""
     from oracle import logprob as O_lp
+    from oracle import path as O_path
+    from oracle import scatter as O_sc
     rec = synth.make_records(traj, 0, n_env_sample)
     x = logits_rows_fn(n_env_sample)                         # float64 [rows, V]
     rows = synth.record_rows(rec, cfg, n_env_sample)
@@ -518,13 +534,30 @@ def oracle_sample_step(cfg, traj, logits_rows_fn, n_env_sample):
     recd = dict(env_id=rec.env_id, step=rec.step, version=rec.version, reward=rec.reward,
                 done=rec.done, value=rec.value, tokens=rec.tokens, logp_behav=lb.astype(np.float32))
     chunks = [{k: v[sl] for k, v in recd.items()} for sl in synth.arrival_chunks(rec.n)]
-    params = dict(n_env=n_env_sample, t_steps=cfg.t_steps, a_tok=cfg.a_tok,
-                  cur_version=synth.CUR_VERSION, max_staleness=1, mode=cfg.adv_mode,
-                  group_of_env=traj.group_id[:n_env_sample], last_value=traj.last_value[:n_env_sample],
-                  whiten=cfg.whiten)
-    t = time.perf_counter()
-    O_path.rollout_to_loss(params, chunks, x)
-    return time.perf_counter() - t
+    t0 = time.perf_counter()
+    buf = O_sc.new_buffer(n_env_sample, cfg.t_steps, cfg.a_tok)
+    seq = 1
+    for ch in chunks:
+        O_sc.scatter_steps(buf, ch, synth.CUR_VERSION, seq)
+        seq += len(ch["env_id"])
+    t1 = time.perf_counter()
+    adv = O_path.advantages(buf, traj.last_value[:n_env_sample], mode=cfg.adv_mode, whiten=cfg.whiten,
+                            group_of_env=traj.group_id[:n_env_sample], cur_version=synth.CUR_VERSION,
+                            max_staleness=1)
+    t2 = time.perf_counter()
+    tv = O_path.token_view(buf, adv["adv"], cfg.a_tok, synth.CUR_VERSION)
+    n_tok = float(adv["counts"]["n_tok"])
+    if pool is None:
+        O_path.loss_and_grad(x, tv, n_tok=n_tok)
+    else:
+        assert _ORACLE_X.shape == x.shape and np.shares_memory(_ORACLE_X, x), \
+            "the pool must be forked after _ORACLE_X is set"
+        R = x.shape[0]
+        cuts = np.linspace(0, R, nproc + 1).astype(int)
+        parts = pool.map(_oracle_rows, [(int(a), int(b), n_tok, tv) for a, b in zip(cuts, cuts[1:])])
+        _ = {k: sum(p[k] for p in parts) for k in parts[0] if k != "denom"}   # fixed order
+    t3 = time.perf_counter()
+    return {"s1": t1 - t0, "s2": t2 - t1, "s3s4": t3 - t2, "total": t3 - t0}
 
 
 def host_cpu() -> str:
@@ -541,14 +574,32 @@ def host_cpu() -> str:
 
 
 def cpu_baseline(cfg, traj, logits, lb_fn=None, n_env_sample=2):
+    """The oracle (as it stands) on the GPU box's host cores: one thread, then all logical
+    cores (S3+S4 row blocks over a fork pool, fixed-order combine), per stage."""
+    import multiprocessing as mp
+    global _ORACLE_X
+    x64 = logits[: n_env_sample * cfg.t_steps * cfg.a_tok].double().cpu().numpy()
+
     def rows_fn(n):
-        return logits[: n * cfg.t_steps * cfg.a_tok].double().cpu().numpy()
-    sec = oracle_sample_step(cfg, traj, rows_fn, n_env_sample)
+        return x64[: n * cfg.t_steps * cfg.a_tok]
+    oracle_sample_step(cfg, traj, rows_fn, 1)          # warm-up (imports, first-call costs)
+    one = oracle_sample_step(cfg, traj, rows_fn, n_env_sample)
+    nproc = os.cpu_count() or 1
+    _ORACLE_X = rows_fn(n_env_sample)    # inherited by the forked workers
+    with mp.get_context("fork").Pool(nproc) as pool:
+        allc = oracle_sample_step(cfg, traj, rows_fn, n_env_sample, pool=pool, nproc=nproc)
+    _ORACLE_X = None
     units = n_env_sample * cfg.n_es
-    return {"value": units / sec, "unit": UNIT, "cores": 1, "kind": "oracle", "host": host_cpu(),
+    stages = lambda d: {k: round(v, 4) for k, v in d.items()}  # noqa: E731
+    return {"value": units / one["total"], "unit": UNIT, "cores": 1, "kind": "oracle", "host": host_cpu(),
             "sample": f"{n_env_sample} of {cfg.n_env} envs x {cfg.n_es} env steps "
                       f"({n_env_sample * cfg.t_steps * cfg.a_tok} logit rows x {cfg.vocab}), "
-                      f"whole path S1-S4, numpy fp64 single thread, {sec:.1f} s"}
+                      f"whole path S1-S4, numpy fp64 single thread, {one['total']:.1f} s",
+            "stage_seconds": stages(one),
+            "all_cores": {"value": units / allc["total"], "unit": UNIT, "cores": nproc,
+                          "stage_seconds": stages(allc),
+                          "how": "same sample; S3+S4 split into row blocks over a fork pool of "
+                                 "every logical core, statistics combined in block order; S1/S2 serial"}}
 
 
 def run_reference(args):
@@ -565,7 +616,8 @@ def run_reference(args):
 
     for _ in range(args.warmup):
         oracle_sample_step(cfg, traj, rows_fn, n)
-    secs = [oracle_sample_step(cfg, traj, rows_fn, n) for _ in range(args.steps)]
+    runs = [oracle_sample_step(cfg, traj, rows_fn, n) for _ in range(args.steps)]
+    secs = [r["total"] for r in runs]
     tot = float(sum(secs))
     value = n * cfg.n_es * args.steps / tot
     sample = (f"{n} of {cfg.n_env} envs x {cfg.n_es} env steps per step "
@@ -577,7 +629,9 @@ def run_reference(args):
            "config": {"workload": cfg.name, "envs_per_step": n, "vocab": cfg.vocab,
                       "parallelism": "cpu oracle (rank 0 only)"},
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "host": host_cpu(),
-                            "sample": sample},
+                            "sample": sample,
+                            "stage_seconds": {k: round(float(np.mean([r[k] for r in runs])), 4)
+                                              for k in ("s1", "s2", "s3s4", "total")}},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "gpu_launches": 0}
     print(json.dumps(out), flush=True)

@@ -61,6 +61,10 @@ def test_fullsize_scatter_and_advantages(full):
 
 
 def test_fullsize_sampled_rows_match_oracle(full):
+    """Sampled rows of the bench's launch vs the oracle chain: the GPU ran on its own
+    advantages and N_tok, the oracle on its own (S2's tolerance propagated into S3/S4 as in
+    tests/test_parity_path.py; nothing crosses between the chains)."""
+    from tests.test_parity_path import _compare_rows
     case = full["case"]
     cfg = case.cfg
     A = cfg.a_tok
@@ -69,16 +73,16 @@ def test_fullsize_sampled_rows_match_oracle(full):
     rows = np.unique(np.concatenate([rng.choice(full["dx"].shape[0], 1024, replace=False), crafted,
                                      np.asarray(case.extra["behav_rows"][:256])]))
     oadv = H.oracle_advantages(case, full["obuf"], "grpo")
-    a32 = full["adv"].cpu().numpy().astype(np.float64)   # S4 compared on the GPU's own adv,
-    H.assert_close_rel(a32, oadv["adv"], 1e-5, 1e-3, "adv")  # which matched the oracle above
-    tv = O_path.token_view(full["obuf"], a32, A, synth.CUR_VERSION)
-    x = case.logits[torch.from_numpy(rows).cuda()].double().cpu().numpy()
-    ref = O_path.loss_and_grad(x, tv, n_tok=full["stats"][3].item(), rows=rows)
-    H.assert_close_rel(full["logp"].cpu().numpy()[rows], ref["fwd"]["logp"], 1e-5, 1.0, "logp")
-    nt = ref["ppo"]["near_tie"]
-    H.assert_close_rel(full["g"].cpu().numpy()[rows][~nt], ref["ppo"]["grad"][~nt], 1e-5, 1e-9, "grad")
-    bits = full["dx"][torch.from_numpy(rows).cuda()].view(torch.int16).cpu().numpy().astype(np.int32) & 0xFFFF
-    H.assert_bf16_ulp(bits[~nt], ref["dx"][~nt], 1)
+    floor = max(1e-3, float(np.sqrt(np.mean(oadv["adv"] ** 2))))
+    tol_tok = np.repeat((1e-5 * np.maximum(np.abs(oadv["adv"]), floor)).reshape(-1), A)
+    tv = O_path.token_view(full["obuf"], oadv["adv"], A, synth.CUR_VERSION)
+    out = {k: full[k].cpu().numpy() for k in ("logp", "lse", "g", "lt")}
+    out["dx"] = full["dx"]
+    n_tok = float(oadv["counts"]["n_tok"])
+    assert full["stats"][3].item() == n_tok
+    for s in range(0, len(rows), 512):
+        rr = rows[s:s + 512]
+        _compare_rows(case, out, tv, rr, n_tok, tol_tok[rr])
 
 
 def test_fullsize_properties(full):

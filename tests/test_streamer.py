@@ -38,7 +38,14 @@ def test_streamer_equals_full_batch(cfg_name, n_env):
     obuf, _ = H.oracle_scatter(case)
     oadv = H.oracle_advantages(case, obuf, "grpo")
     A, T = cfg.a_tok, cfg.t_steps
-    adv = torch.from_numpy(oadv["adv"].astype(np.float32)).cuda()
+    # the GPU chain's own advantages (GRPO: fp32 rounding of the oracle's, checked here)
+    adv = torch.zeros(n_env, T, device="cuda")
+    P.rlvla_advantages(buf, None, P.adv_params("grpo", group_id=torch.from_numpy(case.traj.group_id).cuda(),
+                                               group_size=cfg.group_size, n_env_global=n_env,
+                                               cur_version=synth.CUR_VERSION),
+                       adv, torch.zeros(n_env, T, device="cuda"),
+                       torch.zeros(24, dtype=torch.float64, device="cuda"), P.workspace(n_env))
+    H.assert_close_rel(adv.cpu().numpy(), oadv["adv"], 1e-5, 1e-3, "adv")
     x = case.logits.cuda()
     tgt = buf.tokens.view(-1)
     R = x.shape[0]
@@ -58,7 +65,7 @@ def test_streamer_equals_full_batch(cfg_name, n_env):
     np.testing.assert_allclose(b[6:18], a[6:18], rtol=1e-12, atol=1e-15)
     assert b[18] == a[18] == N
     # and the accumulated stats equal the oracle's
-    tv = O_path.token_view(obuf, oadv["adv"].astype(np.float32).astype(np.float64), A, synth.CUR_VERSION)
+    tv = O_path.token_view(obuf, oadv["adv"], A, synth.CUR_VERSION)
     tot = {}
     for s in range(0, R, 2048):
         rr = np.arange(s, min(R, s + 2048))
