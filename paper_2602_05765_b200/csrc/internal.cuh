@@ -124,6 +124,17 @@ __device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
 }
 
 // packed bf16x2 max that propagates NaN (HMNMX2.NAN)
+// packed bf16x2 products with one rounding each (HMUL2 / HFMA2 .BF16): a*b, a*b + c
+__device__ __forceinline__ uint32_t bmul2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t bfma2(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
 __device__ __forceinline__ uint32_t bmax2_nan(uint32_t a, uint32_t b) {
   __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&a);
   __nv_bfloat162 y = *reinterpret_cast<__nv_bfloat162*>(&b);
@@ -360,7 +371,7 @@ struct LpArgs {
   double* stats;
   Workspace ws;
 };
-enum LpPath { LP_PATH_TMA = 0, LP_PATH_WARP = 1, LP_PATH_GENERIC = 2 };
+enum LpPath { LP_PATH_TMA = 0, LP_PATH_WARP = 1, LP_PATH_GENERIC = 2, LP_PATH_ROW = 3 };
 LpPath select_lp_path(const LpArgs& a);
 cudaError_t launch_logprob(const LpArgs& a, cudaStream_t s);
 

@@ -20,12 +20,21 @@ namespace {
 
 enum { MODE_FWD = 0, MODE_FUSED = 1, MODE_BWD = 2 };
 
-// build-time variants for A/B timing (tools/ab_variants.py); defaults are the product.
-#ifndef RLVLA_NFULL_FUSED
-#define RLVLA_NFULL_FUSED 0  // A/B: unchecked vectors cost the fused kernel 4-5% (one spill at 64 regs)
-#endif
 // (Measured and rejected: a NaN-guarded per-vector redo instead of the per-element -inf
 // clamp in the entropy partial — 4% slower, the per-vector branch costs more than it saves.)
+// build-time switches for A/B timing (tools/ab_variants.py); defaults are the product
+#ifndef RLVLA_TGT_INLOOP
+#define RLVLA_TGT_INLOOP 0  // 1: the target dlogit merged into its vector inside pass C
+#endif
+#ifndef RLVLA_FUSED_NEGINF
+#define RLVLA_FUSED_NEGINF 1  // 0: the fused kernel skips the target inside the pass-B loop
+#endif
+#ifndef RLVLA_PASSC_BF16
+#define RLVLA_PASSC_BF16 1  // 0: pass C in fp32 (unpack, FMUL2, pack) instead of bf16 HFMA2
+#endif
+#ifndef RLVLA_NFULL_FUSED
+#define RLVLA_NFULL_FUSED 1  // 0: every vector of the fused kernel bounds-checked
+#endif
 
 constexpr uint32_t kNegClampPair = 0xF180F180u;  // bf16x2 (-2^100, -2^100)
 
@@ -310,7 +319,11 @@ __device__ __forceinline__ void scalars_sync(int g) {
 // no code of the other.
 // NFULL: the first NFULL of a thread's kVecPerThread vectors are always inside the row
 // (NFULL = nvec / 512), so those iterations carry no bounds check.
-template <int MODE, bool XP, int NFULL>
+// DX: dlogits requested (FUSED); compile-time so that no per-vector test reloads it.
+// Every per-vector loop is branch-free: the target column is overwritten with -inf after
+// pass A (removed from the pass-B sums, 0 in pass C) and its dlogit is stored by its owner
+// thread after the row's vectors; a row without gradient takes a store-zeros loop.
+template <int MODE, bool XP, int NFULL, bool DX>
 __global__ void __launch_bounds__(kCtaThreads, 1)
     lp_tma_kernel(Lp p, int nstages, uint32_t stage_bytes) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -336,14 +349,12 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
   // pass C runs in external-bwd mode and in fused mode with dlogits; it reuses the e
   // values of pass B (stored as bf16 in the stage) unless the entropy bonus needs x
   constexpr bool kXPath = XP || MODE == MODE_BWD;
-  // forward: the target column is removed from the pass-B sums by overwriting it with -inf
-  // after pass A (branch-free loop); fused: skipped inside the loop of its owner thread
-#ifndef RLVLA_NEGINF_FUSED
-#define RLVLA_NEGINF_FUSED 0
-#endif
-  constexpr bool kNegInfTarget = MODE == MODE_FWD || (MODE == MODE_FUSED && RLVLA_NEGINF_FUSED);
-  const bool has_c = MODE == MODE_BWD || (MODE == MODE_FUSED && p.dx != nullptr);
-  const bool keep_e = MODE == MODE_FUSED && !kXPath && p.dx != nullptr;
+  constexpr bool has_c = MODE == MODE_BWD || (MODE == MODE_FUSED && DX);
+  // the target column removed from the pass-B sums by a -inf overwrite after pass A (else,
+  // an A/B variant, skipped inside the loop by its owner; either way its dlogit is stored
+  // from ga)
+  constexpr bool kNegInf = MODE != MODE_FUSED || RLVLA_FUSED_NEGINF;
+  constexpr bool keep_e = MODE == MODE_FUSED && !kXPath && DX;
   const float L2E = kLog2e;
 
   if (tid == 0) {
@@ -403,7 +414,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
       // The target column is excluded from the pass-B sums (so that 1 - p_a = S_rest / S
       // keeps full relative precision near saturation) by overwriting it with -inf in the
       // stage once the max has seen it; only its owner thread reads that vector again.
-      if (kNegInfTarget && owner) {
+      if (kNegInf && owner) {
         uint16_t* hx = reinterpret_cast<uint16_t*>(row);
         *gxa = bf_lo(uint32_t(hx[a]));
         hx[a] = 0xFF80u;
@@ -431,15 +442,13 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
             t2[q] = __ffma2_rn(make_float2(bf_lo(c), bf_hi(c)), L2E2, nmL2);
             e2[q] = make_float2(ex2(t2[q].x), ex2(t2[q].y));
           }
-          if (kNegInfTarget || idx != va) {
+          if (kNegInf || idx != va) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               s2 = __fadd2_rn(s2, e2[q]);
               et2 = __ffma2_rn(e2[q], t2[q], et2);
             }
-          } else {
-            // fused kernel: the target column is skipped here instead (A/B: the -inf
-            // overwrite costs the fused kernel ~1.5%, it saves the forward 11%)
+          } else {  // (A/B variant) the target column skipped here instead
             const int j0 = a & 7;
             const int h = j0 >> 1;
             const uint32_t wa = h == 0 ? w.x : (h == 1 ? w.y : (h == 2 ? w.z : w.w));
@@ -532,24 +541,37 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     // ---- pass C: dlogits (masked / clipped rows get exact zeros) ---------------------
     {
       __nv_bfloat16* drow = static_cast<__nv_bfloat16*>(p.dx) + int64_t(r) * p.ld;
-      const float kw = !kXPath ? rsv.k1 * ex2((mws - rsv.M) * L2E) : rsv.k1;
-      const float nML = -rsv.M * L2E;
+      uint4* dv = reinterpret_cast<uint4*>(drow);
+      if (rsv.active != 0.f) {
+        const float kw = !kXPath ? rsv.k1 * ex2((mws - rsv.M) * L2E) : rsv.k1;
+        const float nML = -rsv.M * L2E;
+        // kw split into two bf16 halves, each broadcast to both lanes of a pair
+        const uint32_t kwh1 = uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(kw)));
+        const uint32_t kwl1 = uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(kw - __uint_as_float(kwh1 << 16))));
+        const uint32_t kwh2 = kwh1 | (kwh1 << 16), kwl2 = kwl1 | (kwl1 << 16);
 #pragma unroll
-      for (int i = 0; i < kVecPerThread; ++i) {
-        const int idx = gt + i * kGroupThreads;
-        if (i < NFULL || idx < nvec) {
-          uint4 o = make_uint4(0u, 0u, 0u, 0u);
-          if (rsv.active != 0.f) {
+        for (int i = 0; i < kVecPerThread; ++i) {
+          const int idx = gt + i * kGroupThreads;
+          if (i < NFULL || idx < nvec) {
             const uint4 w = rv[idx];
             const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
+            uint4 o;
             uint32_t* ow = &o.x;
             if (!kXPath) {
-              // FUSED: dx = g' 2^{(m_w - M) log2e} e, e from pass B (bf16 in SMEM)
+              // FUSED: dx = kw e, kw = g' 2^{(m_w - M) log2e}, e from pass B (bf16 in SMEM),
+              // on the packed pairs: kw = kw_hi + kw_lo (both bf16), dx = RN(e kw_hi + RN(e kw_lo));
+              // the inner rounding is <= 2^-18 |e kw|, so dx stays within one bf16 ulp of
+              // RNE(e kw) -> within one ulp of RNE(exact) as before
+#if RLVLA_PASSC_BF16
+#pragma unroll
+              for (int q = 0; q < 4; ++q) ow[q] = bfma2(w4[q], kwh2, bmul2(w4[q], kwl2));
+#else
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 const float2 d = __fmul2_rn(make_float2(bf_lo(w4[q]), bf_hi(w4[q])), make_float2(kw, kw));
                 ow[q] = pack_bf16x2(d.x, d.y);
               }
+#endif
             } else {
               // from x: t = (x - M) log2e (lse in external bwd), dx = 2^t (k1 + k2 t);
               // -inf columns are clamped per bf16 pair so that t stays finite
@@ -566,6 +588,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
                 ow[q] = pack_bf16x2(d2.x, d2.y);
               }
             }
+#if RLVLA_TGT_INLOOP
             if (idx == va) {  // the target column (0 from its -inf) takes g (1 - p_a) [+ ...]
               const uint32_t hb = uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(rsv.ga)));
               const int qd = (a & 7) >> 1, hf = a & 1;
@@ -573,8 +596,20 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
               for (int z = 0; z < 4; ++z)
                 if (z == qd) ow[z] = hf ? ((ow[z] & 0x0000ffffu) | (hb << 16)) : ((ow[z] & 0xffff0000u) | hb);
             }
+#endif
+            stg_stream(dv + idx, o);
           }
-          stg_stream(reinterpret_cast<uint4*>(drow) + idx, o);
+        }
+#if !RLVLA_TGT_INLOOP
+        // the target column (0 from its -inf above) takes g (1 - p_a) [+ ...]: stored by
+        // the thread that stored its vector, after it (same-thread order)
+        if (owner) reinterpret_cast<uint16_t*>(drow)[a] = __bfloat16_as_ushort(__float2bfloat16_rn(rsv.ga));
+#endif
+      } else {
+#pragma unroll
+        for (int i = 0; i < kVecPerThread; ++i) {
+          const int idx = gt + i * kGroupThreads;
+          if (i < NFULL || idx < nvec) stg_stream(dv + idx, make_uint4(0u, 0u, 0u, 0u));
         }
       }
     }
@@ -810,6 +845,202 @@ __global__ void __launch_bounds__(256) lp_generic_kernel(Lp p) {
   }
 }
 
+// =====================================================================================
+// Aligned rows the TMA kernel cannot stage (fp32 logits with V > 2048, bf16 with V > 32768):
+// one 512-thread CTA per row (4 CTAs per SM), 16-byte loads. Pass AB reads the row once with
+// an online (max, sum, entropy) per thread — the thread's partial sums are rescaled when its
+// max grows — then a CTA combine and the per-row epilogue; pass C re-reads the row (an L2
+// hit: the row was read microseconds before) and writes dlogits with dx = 2^t (k1 + k2 t),
+// t = (x - M) log2e, i.e. one DRAM read and one write per element. (The earlier path for
+// these rows, lp_generic_kernel, made three scalar passes.)
+// =====================================================================================
+constexpr int kRowThreads = 512;
+
+template <typename T>
+struct RowVec;
+template <>
+struct RowVec<float> {
+  static constexpr int kN = 4;
+  __device__ __forceinline__ static void load(const void* row, int v, float (&x)[4]) {
+    const uint4 w = ldg_stream(reinterpret_cast<const uint4*>(row) + v);
+    x[0] = __uint_as_float(w.x);
+    x[1] = __uint_as_float(w.y);
+    x[2] = __uint_as_float(w.z);
+    x[3] = __uint_as_float(w.w);
+  }
+  __device__ __forceinline__ static void store(void* row, int v, const float (&d)[4]) {
+    stg_stream(reinterpret_cast<uint4*>(row) + v,
+               make_uint4(__float_as_uint(d[0]), __float_as_uint(d[1]), __float_as_uint(d[2]), __float_as_uint(d[3])));
+  }
+};
+template <>
+struct RowVec<__nv_bfloat16> {
+  static constexpr int kN = 8;
+  __device__ __forceinline__ static void load(const void* row, int v, float (&x)[8]) {
+    const uint4 w = ldg_stream(reinterpret_cast<const uint4*>(row) + v);
+    const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      x[2 * q] = bf_lo(w4[q]);
+      x[2 * q + 1] = bf_hi(w4[q]);
+    }
+  }
+  __device__ __forceinline__ static void store(void* row, int v, const float (&d)[8]) {
+    stg_stream(reinterpret_cast<uint4*>(row) + v,
+               make_uint4(pack_bf16x2(d[0], d[1]), pack_bf16x2(d[2], d[3]), pack_bf16x2(d[4], d[5]),
+                          pack_bf16x2(d[6], d[7])));
+  }
+};
+
+// merge (m, s, et) partials: s = sum 2^{(x - m) log2e}, et = sum e t with t relative to m
+__device__ __forceinline__ void lse_merge(float& m, float& s, float& et, float m2, float s2, float et2) {
+  const float M = fmaxf(m, m2);
+  if (M == -INFINITY) return;  // both empty
+  const float d1 = (m == -INFINITY) ? 0.f : (m - M) * kLog2e;
+  const float d2 = (m2 == -INFINITY) ? 0.f : (m2 - M) * kLog2e;
+  const float f1 = (m == -INFINITY) ? 0.f : ex2(d1), f2 = (m2 == -INFINITY) ? 0.f : ex2(d2);
+  et = f1 * fmaf(d1, s, et) + f2 * fmaf(d2, s2, et2);
+  s = f1 * s + f2 * s2;
+  m = M;
+}
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kRowThreads, 4) lp_row_kernel(Lp p) {
+  constexpr int VN = RowVec<T>::kN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int V = p.V;
+  const int nvec = V / VN;
+  const float L2E = kLog2e;
+  const bool want_stats = p.stats != nullptr && MODE != MODE_BWD;
+  PpoConst pc;
+  const double Nden = resolve_pc<MODE>(p, pc);
+  __shared__ float4 red[kRowThreads / 32];
+  __shared__ RowScalars rsc;
+  __shared__ double sacc[16];
+  if (tid < 16) sacc[tid] = 0.0;
+  __syncthreads();
+  for (int64_t r = blockIdx.x; r < p.rows; r += gridDim.x) {
+    const T* xr = static_cast<const T*>(p.x) + r * p.ld;
+    const int a = p.target[r];
+    const bool tgt_ok = unsigned(a) < unsigned(V);
+    const int va = tgt_ok ? a / VN : -1;
+    float Ms = 0.f;
+    if (MODE != MODE_BWD) {
+      // ---- pass AB: online max / sum / entropy partial, the target column left out ------
+      float m = -INFINITY, sm = 0.f, et = 0.f;
+      for (int v = tid; v < nvec; v += kRowThreads) {
+        float x[VN];
+        RowVec<T>::load(xr, v, x);
+        if (v == va) x[a - va * VN] = -INFINITY;
+        float lm = x[0];
+#pragma unroll
+        for (int j = 1; j < VN; ++j) lm = fmaxf(lm, x[j]);
+        if (lm > m) {  // the thread's max grows: rescale its partials
+          const float d = (m == -INFINITY) ? 0.f : (m - lm) * L2E;
+          const float f = (m == -INFINITY) ? 0.f : ex2(d);
+          et = f * fmaf(d, sm, et);
+          sm = f * sm;
+          m = lm;
+        }
+        const float nmL = (m == -INFINITY) ? 0.f : -m * L2E;
+#pragma unroll
+        for (int j = 0; j < VN; ++j) {
+          const float t = clamp_ninf(fmaf(x[j], L2E, nmL));
+          const float e = ex2(t);
+          sm += e;
+          et = fmaf(e, fmaxf(t, -256.f), et);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+        lse_merge(m, sm, et, __shfl_xor_sync(0xffffffffu, m, o), __shfl_xor_sync(0xffffffffu, sm, o),
+                  __shfl_xor_sync(0xffffffffu, et, o));
+      if (lane == 0) red[warp] = make_float4(m, sm, et, 0.f);
+      __syncthreads();
+      if (warp == 0) {
+        const float4 q = lane < kRowThreads / 32 ? red[lane] : make_float4(-INFINITY, 0.f, 0.f, 0.f);
+        float M = q.x, Srest = q.y, Cs = q.z;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1)
+          lse_merge(M, Srest, Cs, __shfl_xor_sync(0xffffffffu, M, o), __shfl_xor_sync(0xffffffffu, Srest, o),
+                    __shfl_xor_sync(0xffffffffu, Cs, o));
+        const float xa = tgt_ok ? to_f<T>(xr[a]) : 0.f;
+        // the row max over every column (the target included), sums referred to it
+        float Mrow = fmaxf(M, tgt_ok ? xa : -INFINITY);
+        if (Mrow != M && M != -INFINITY) {
+          const float d = (M - Mrow) * L2E, f = ex2(d);
+          Cs = f * fmaf(d, Srest, Cs);
+          Srest = f * Srest;
+        }
+        if (isnan(xa)) Mrow = xa;
+        const float Mz = (Mrow == -INFINITY) ? 0.f : Mrow;
+        const float ta = (xa - Mz) * L2E;
+        const float ea = tgt_ok ? ex2(ta) : 0.f;
+        const float Stot = Srest + ea;
+        const LseParts lp = lse_parts(xa, Mz, Stot);
+        const float lnS = lp.lnS;
+        const float lse_row = Mz + lnS;
+        const float logp = lp.logp;
+        const float invS = __fdividef(1.f, Stot);
+        const float H = lnS - (Cs + (tgt_ok ? ea * fmaxf(ta, -256.f) : 0.f)) * invS * kLn2;
+        const RowMeta rm = load_meta<MODE>(p, r);
+        RowOut ro;
+        const RowGrad rg = eval_row<MODE>(p, pc, a, lse_row, logp, H, rm, ro);
+        if (lane == 0) {
+          RowScalars s4;
+          s4.M = Mz;
+          s4.k1 = (-rg.g + rg.c * (H - lnS)) * invS;
+          s4.k2 = rg.c * kLn2 * invS;
+          s4.ga = target_grad(rg, Srest, ea, invS, logp, H);
+          s4.active = (rg.g != 0.f || rg.c != 0.f) ? 1.f : 0.f;
+          rsc = s4;
+          write_row<MODE>(p, pc, r, rg, ro, want_stats ? sacc : nullptr);
+        }
+      }
+      __syncthreads();
+      Ms = rsc.M;
+    } else if (tid == 0) {
+      const float g = tgt_ok ? p.g_in[r] : 0.f;
+      RowScalars s4;
+      s4.M = p.lse_in[r];
+      s4.k1 = -g;
+      s4.k2 = 0.f;
+      s4.ga = tgt_ok ? -g * expm1f(to_f<T>(xr[a]) - s4.M) : 0.f;
+      s4.active = g != 0.f ? 1.f : 0.f;
+      rsc = s4;
+    }
+    if (MODE != MODE_FWD && p.dx != nullptr) {
+      if (MODE == MODE_BWD) __syncthreads();
+      const RowScalars sc = rsc;
+      (void)Ms;
+      T* dr = static_cast<T*>(p.dx) + r * p.ld;
+      const float nML = -sc.M * L2E;
+      for (int v = tid; v < nvec; v += kRowThreads) {
+        float d[VN];
+        if (sc.active != 0.f) {
+          float x[VN];
+          RowVec<T>::load(xr, v, x);
+#pragma unroll
+          for (int j = 0; j < VN; ++j) {
+            const float t = clamp_ninf(fmaf(x[j], L2E, nML));
+            d[j] = ex2(t) * fmaf(sc.k2, t, sc.k1);
+          }
+          if (v == va) d[a - va * VN] = sc.ga;
+        } else {
+#pragma unroll
+          for (int j = 0; j < VN; ++j) d[j] = 0.f;
+        }
+        RowVec<T>::store(dr, v, d);
+      }
+    }
+    __syncthreads();  // red / rsc reuse across rows
+  }
+  if (want_stats) {
+    __syncthreads();
+    finish_loss_stats(sacc, p.stats, p.partials, p.ctrl, Nden, p.accumulate, pc.ent_coef, &p.p2p);
+  }
+}
+
 Lp make_lp(const LpArgs& a) {
   Lp p{};
   p.x = a.x.ptr;
@@ -872,18 +1103,23 @@ cudaError_t launch_mode(const LpArgs& a, Lp p, cudaStream_t s) {
     // dynamic smem limit = opt-in max minus the kernel's static smem
     const bool xp = MODE == MODE_FUSED && a.f.ent_coef != 0.f && a.dlogits != nullptr;
     const int nvec = a.x.vocab >> 3;
-    // V > 28672 (OpenVLA 32000): 7 unchecked vectors (RLVLA_NFULL_FUSED=0 keeps the checks in
-    // the fused kernel)
+    // V > 28672 (OpenVLA 32000): 7 unchecked vectors
     const bool f7 = nvec / kGroupThreads >= 7 && (MODE != MODE_FUSED || RLVLA_NFULL_FUSED);
-    const void* fn = xp ? (f7 ? reinterpret_cast<const void*>(lp_tma_kernel<MODE, true, 7>)
-                              : reinterpret_cast<const void*>(lp_tma_kernel<MODE, true, 0>))
-                        : (f7 ? reinterpret_cast<const void*>(lp_tma_kernel<MODE, false, 7>)
-                              : reinterpret_cast<const void*>(lp_tma_kernel<MODE, false, 0>));
+    const bool dx = MODE == MODE_FUSED && a.dlogits != nullptr;
+    // kernel instance: [xp][f7][dx]
+    using Fn = void (*)(Lp, int, uint32_t);
+    constexpr bool kDx = MODE != MODE_FWD;  // FWD never writes dlogits
+    Fn fns[2][2][2] = {{{lp_tma_kernel<MODE, false, 0, false>, lp_tma_kernel<MODE, false, 0, kDx>},
+                        {lp_tma_kernel<MODE, false, 7, false>, lp_tma_kernel<MODE, false, 7, kDx>}},
+                       {{lp_tma_kernel<MODE, true, 0, false>, lp_tma_kernel<MODE, true, 0, kDx>},
+                        {lp_tma_kernel<MODE, true, 7, false>, lp_tma_kernel<MODE, true, 7, kDx>}}};
+    const Fn kern = fns[xp][f7][MODE == MODE_BWD ? 1 : (dx ? 1 : 0)];
+    const void* fn = reinterpret_cast<const void*>(kern);
     // the opt-in SMEM limit is a per-device function attribute: cached per device
-    static int attr_dyn[kMaxDevices][3][2][2] = {};
+    static int attr_dyn[kMaxDevices][3][2][2][2] = {};
     const int dev = device_info().device;
     int dummy = 0;
-    int& cached = (dev >= 0 && dev < kMaxDevices) ? attr_dyn[dev][MODE][xp][f7] : dummy;
+    int& cached = (dev >= 0 && dev < kMaxDevices) ? attr_dyn[dev][MODE][xp][f7][dx] : dummy;
     if (cached < int(smem)) {
       cudaFuncAttributes fa{};
       cudaError_t e = cudaFuncGetAttributes(&fa, fn);
@@ -895,13 +1131,7 @@ cudaError_t launch_mode(const LpArgs& a, Lp p, cudaStream_t s) {
     }
     const int psms = persistent_sms();
     int grid = int(R < psms ? R : psms);
-    if (xp) {
-      if (f7) lp_tma_kernel<MODE, true, 7><<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);
-      else lp_tma_kernel<MODE, true, 0><<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);
-    } else {
-      if (f7) lp_tma_kernel<MODE, false, 7><<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);
-      else lp_tma_kernel<MODE, false, 0><<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);
-    }
+    kern<<<grid, kCtaThreads, smem, s>>>(p, nst, stage_bytes);
     return cudaGetLastError();
   }
   if (path == LP_PATH_WARP) {
@@ -920,6 +1150,14 @@ cudaError_t launch_mode(const LpArgs& a, Lp p, cudaStream_t s) {
       else if (nv <= 4) lp_warp_kernel<float, 4, MODE><<<g, 256, 0, s>>>(p);
       else lp_warp_kernel<float, 8, MODE><<<g, 256, 0, s>>>(p);
     }
+    return cudaGetLastError();
+  }
+  if (path == LP_PATH_ROW) {
+    int64_t blocks = R;
+    const int64_t cap = int64_t(sms) * 4;
+    if (blocks > cap) blocks = cap;
+    if (a.x.dtype == RLVLA_BF16) lp_row_kernel<__nv_bfloat16, MODE><<<int(blocks), kRowThreads, 0, s>>>(p);
+    else lp_row_kernel<float, MODE><<<int(blocks), kRowThreads, 0, s>>>(p);
     return cudaGetLastError();
   }
   int64_t blocks = R;
@@ -942,7 +1180,7 @@ LpPath select_lp_path(const LpArgs& a) {
   if (V <= 32 * 8 * VW && V / VW <= 256) return LP_PATH_WARP;
   if (a.x.dtype == RLVLA_BF16 && V <= kGroupThreads * kVecPerThread * 8 && a.x.rows < (int64_t(1) << 31))
     return LP_PATH_TMA;
-  return LP_PATH_GENERIC;
+  return LP_PATH_ROW;
 }
 
 cudaError_t launch_logprob(const LpArgs& a, cudaStream_t s) {

@@ -95,6 +95,14 @@ def test_guards_core_path():
     P.rlvla_logprob_fwd_bwd(x, t, logp=lp, lse=ls2)
     P.rlvla_logprob_fwd_bwd(x, t, lse=ls2, grad_logp=torch.ones(19, device="cuda"), dlogits=dx)
     gd.check("generic")
+    # row path: aligned fp32 beyond the warp kernel, fused with PPO statistics
+    x = torch.randn(21, 8192, device="cuda")
+    t = torch.randint(-1, 8192, (21,), device="cuda", dtype=torch.int32)
+    lp, ls2 = gd((21,), torch.float32), gd((21,), torch.float32)
+    dx = gd((21, 8192), torch.float32)
+    P.rlvla_logprob_fwd_bwd(x, t, logp=lp, lse=ls2)
+    P.rlvla_logprob_fwd_bwd(x, t, lse=ls2, grad_logp=torch.ones(21, device="cuda"), dlogits=dx)
+    gd.check("row")
 
 
 @pytest.mark.parametrize("fifo", [False, True])

@@ -1,5 +1,5 @@
-"""GPU parity for rlvla_logprob_fwd_bwd in all three modes and all three kernel paths
-(warp / TMA / generic), plus rlvla_ppo_loss, against the oracle; crafted edge rows,
+"""GPU parity for rlvla_logprob_fwd_bwd in all three modes and all four kernel paths
+(warp / TMA / row / generic), plus rlvla_ppo_loss, against the oracle; crafted edge rows,
 ragged vocabularies, ignore/bad targets, non-finite rows, in-place dlogits, determinism."""
 import numpy as np
 import pytest
@@ -65,8 +65,10 @@ CASES = [
     (150, 4104, torch.bfloat16, "tma"),
     (150, 32768, torch.bfloat16, "tma"),
     (64, 31999, torch.bfloat16, "generic"),    # ragged: V % 8 != 0
-    (64, 5000, torch.float32, "generic"),
-    (40, 40000, torch.bfloat16, "generic"),
+    (64, 5003, torch.float32, "generic"),      # ragged: V % 4 != 0
+    (64, 5000, torch.float32, "row"),          # aligned fp32 beyond the warp path
+    (300, 32000, torch.float32, "row"),        # fp32 logits at the OpenVLA vocabulary
+    (40, 40000, torch.bfloat16, "row"),        # bf16 beyond the TMA stage
 ]
 
 

@@ -50,7 +50,7 @@ def _case(R, V, dtype, A, seed=0):
 VARIANTS = [dict(dual_clip=3.0), dict(kl_coef=0.05), dict(ent_coef=0.01),
             dict(dual_clip=2.5, kl_coef=0.1, ent_coef=0.02)]
 SHAPES = [(280, 256, torch.float32), (280, 1000, torch.bfloat16), (140, 32000, torch.bfloat16),
-          (56, 5003, torch.float32)]
+          (56, 5003, torch.float32), (56, 8192, torch.float32)]
 
 
 @pytest.mark.parametrize("R,V,dtype", SHAPES)

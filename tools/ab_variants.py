@@ -12,13 +12,13 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
-    "noscan": ("RLVLA_SCATTER_SCAN_MAX=0",),
-    "stop1": ("RLVLA_SCATTER_STOP=1",),
-    "stop2": ("RLVLA_SCATTER_STOP=2",),
+    "noneg": ("RLVLA_FUSED_NEGINF=0",),
+    "fp32c": ("RLVLA_PASSC_BF16=0",),
+    "r1like": ("RLVLA_FUSED_NEGINF=0", "RLVLA_PASSC_BF16=0", "RLVLA_NFULL_FUSED=0", "RLVLA_TGT_INLOOP=1"),
 }
 # name -> git revision whose csrc/ + include/ are built as one more variant
 # (the ABI only grew at the end of its structs, so today's binding drives older libraries)
-REVISIONS = {}  # e.g. {"prev": "HEAD"} builds the last commit as a variant
+REVISIONS = {"prev": os.environ.get("AB_PREV", "HEAD")}  # the last commit as a variant
 
 
 def build_revision(name, rev):
@@ -73,6 +73,9 @@ def run(mode="fused", rounds=3):
                 cmd = [sys.executable, os.path.join(ROOT, "tools", "prof_batcher.py"), "--iters", "30"]
             elif mode == "scatter":
                 cmd = [sys.executable, os.path.join(ROOT, "tools", "prof_scatter.py")]
+            elif mode == "bench":  # the whole bench step (pipelined), at the box's sustained clocks
+                cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--no-cpu-baseline", "--no-e2e",
+                       "--steps", "40"]
             elif mode == "flow":
                 cmd = [sys.executable, os.path.join(ROOT, "tools", "prof_flow.py"), "--rows", "196608"]
                 cmd += os.environ.get("FLOW_ARGS", "").split()  # e.g. "--learned --f32"
@@ -91,6 +94,9 @@ def run(mode="fused", rounds=3):
                 res.setdefault(name, []).append((round(d["us_min"], 1), round(d["us_median"], 1)))
             elif mode == "scatter":
                 res.setdefault(name, []).append(round(d["us_per_call"], 2))
+            elif mode == "bench":
+                res.setdefault(name, []).append((round(d["ms_per_step"], 3), round(d["roofline"]["kernel_ms"], 3),
+                                                 (d.get("clocks") or {}).get("sm_mhz")))
             else:
                 res.setdefault(name, []).append((round(d["ms_min"], 3), round(d["ms_avg"], 3)))
     print(json.dumps(res))

@@ -22,16 +22,19 @@ def main():
     ap.add_argument("--rows", type=int, default=229376)
     ap.add_argument("--vocab", type=int, default=32000)
     ap.add_argument("--A", type=int, default=56)
+    ap.add_argument("--f32", action="store_true", help="fp32 logits (the row kernel at V > 2048)")
     ap.add_argument("--variant", default="none", choices=["none", "dual", "kl", "ent", "all"],
                     help="NEXT-2 loss knobs on the fused call (readings R19-R20)")
     a = ap.parse_args()
     R, V, A = a.rows, a.vocab, a.A
     dev = "cuda"
     g = torch.Generator(device=dev).manual_seed(0)
-    x = torch.empty(R, V, dtype=torch.bfloat16, device=dev)
+    dt = torch.float32 if a.f32 else torch.bfloat16
+    esz = 4 if a.f32 else 2
+    x = torch.empty(R, V, dtype=dt, device=dev)
     for s in range(0, R, 16384):
         n = min(16384, R - s)
-        x[s:s + n] = (torch.randn(n, V, generator=g, device=dev) * 1.5).to(torch.bfloat16)
+        x[s:s + n] = (torch.randn(n, V, generator=g, device=dev) * 1.5).to(dt)
     t = torch.randint(V - 256, V, (R,), generator=g, device=dev, dtype=torch.int32)
     dx = torch.empty_like(x)
     logp = torch.empty(R, device=dev)
@@ -77,7 +80,7 @@ def main():
         ev[i + 1].record()
     torch.cuda.synchronize()
     ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(a.iters)]
-    rw = {"fused": 2 * V * 2 + 12, "fwd": 2 * V + 12, "bwd": 2 * V * 2 + 12}[a.mode]
+    rw = {"fused": 2 * V * esz + 12, "fwd": V * esz + 12, "bwd": 2 * V * esz + 12}[a.mode]
     if a.mode == "fused" and "logp_ref" in vk:
         rw += 4
     byt = R * rw
@@ -88,7 +91,7 @@ def main():
         clip = st[7] / max(1.0, st[11])
     else:
         clip = None
-    print(json.dumps({"mode": a.mode, "variant": a.variant, "rows": R, "vocab": V, "ms_avg": avg, "ms_min": min(ms),
+    print(json.dumps({"mode": a.mode, "variant": a.variant, "rows": R, "vocab": V, "dtype": str(dt), "ms_avg": avg, "ms_min": min(ms),
                       "clip_frac": clip,
                       "GBps_avg": byt / avg / 1e6, "GBps_best": byt / min(ms) / 1e6,
                       "ms_all": [round(v, 3) for v in ms]}))
