@@ -569,6 +569,14 @@ __global__ void __launch_bounds__(WARPS * 32) flow_tma_kernel(FlowArgs a) {
   float* s_isig = reinterpret_cast<float*>(tsm + 8 * kTmaWarps * kFlowStages);
   unsigned char* ring = tsm + tma_ring_offset<NQ, kTmaWarps, kFlowStages>() + size_t(warp) * kFlowStages * stage_b;
   __shared__ double s_lnsig;
+  FlowCtx x = flow_setup<MODE>(a, n, s_isig, kTile * n, &s_lnsig);
+  if (lane == 0) {
+    for (int st = 0; st < kFlowStages; ++st) mbar_init(&bars[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  x.lnsig = s_lnsig;
+  float acc[kLossSlots] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   const int64_t nfull = a.c.rows / kTile;
   const int64_t gw = int64_t(blockIdx.x) * kTmaWarps + warp, nw = int64_t(gridDim.x) * kTmaWarps;
   const int64_t cnt = gw < nfull ? (nfull - gw + nw - 1) / nw : 0;  // this warp's full tiles
@@ -583,18 +591,8 @@ __global__ void __launch_bounds__(WARPS * 32) flow_tma_kernel(FlowArgs a) {
     bulk_g2s(st + kMuB, a.c.x + e0, kXB, bar, pol);
     if (LEARNED) bulk_g2s(st + kMuB + kXB, a.c.log_std + e0, kXB, bar, pol);
   };
-  // the warp's own barriers and first tile loads come first: the per-CTA setup below (the
-  // 1/sigma table, the fp64 ln sigma sum) then overlaps the loads' latency — for one paper-
-  // sized update (~1.3 tiles per warp) that latency is most of the kernel
-  if (lane == 0) {
-    for (int st = 0; st < kFlowStages; ++st) mbar_init(&bars[st], 1);
-    fence_mbar_init();
+  if (lane == 0)
     for (int64_t i = 0; i < cnt && i < kFlowStages; ++i) issue(i);
-  }
-  FlowCtx x = flow_setup<MODE>(a, n, s_isig, kTile * n, &s_lnsig);
-  __syncthreads();
-  x.lnsig = s_lnsig;
-  float acc[kLossSlots] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   float gin;
   RowMeta4 mt_next = load_meta<MODE>(a, x, gw < nfull ? gw * kTile : 0, kTile, lane, gin);
   for (int64_t i = 0; i < cnt; ++i) {

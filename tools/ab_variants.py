@@ -12,9 +12,8 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
-    "noneg": ("RLVLA_FUSED_NEGINF=0",),
-    "fp32c": ("RLVLA_PASSC_BF16=0",),
-    "r1like": ("RLVLA_FUSED_NEGINF=0", "RLVLA_PASSC_BF16=0", "RLVLA_NFULL_FUSED=0", "RLVLA_TGT_INLOOP=1"),
+    "s8x2": ("RLVLA_FLOW_SMALL_TILES=0",),
+    "direct": ("RLVLA_FLOW_TMA=0",),
 }
 # name -> git revision whose csrc/ + include/ are built as one more variant
 # (the ABI only grew at the end of its structs, so today's binding drives older libraries)
