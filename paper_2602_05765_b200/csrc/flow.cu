@@ -543,6 +543,9 @@ __global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(
 // and 16 x 1 for a sigma schedule with fewer than ~4 tiles per warp of the 8 x 2 grid (one
 // update of 24,576 steps: more, shallower warps finish the few tiles sooner) —
 // profiles/r1/FLOW.md
+#ifndef RLVLA_FLOW_16W_MINB
+#define RLVLA_FLOW_16W_MINB 0  // 1: cap the 16-warp shape at 64 registers (2 CTAs per SM; A/B: spills, slower)
+#endif
 #ifndef RLVLA_FLOW_SMALL_TILES
 #define RLVLA_FLOW_SMALL_TILES 9472  // tiles below which the 16 x 1 shape runs (0: never)
 #endif
@@ -558,7 +561,9 @@ __host__ __device__ constexpr int tma_ring_offset() {
 }
 
 template <typename T, int MODE, int NQ, bool LEARNED, int WARPS, int STAGES>
-__global__ void __launch_bounds__(WARPS * 32) flow_tma_kernel(FlowArgs a) {
+// (16-warp CTAs are held to 64 registers so that two fit per SM with their SMEM rings:
+// one paper-sized update then has ~1.3 tiles per warp instead of ~2.6)
+__global__ void __launch_bounds__(WARPS * 32, RLVLA_FLOW_16W_MINB && WARPS == 16 ? 2 : 1) flow_tma_kernel(FlowArgs a) {
   constexpr int kTmaWarps = WARPS, kFlowStages = STAGES;
   constexpr int n = 4 * NQ;
   constexpr int kMuB = kTile * n * int(sizeof(T)), kXB = kTile * n * 4;
@@ -668,6 +673,10 @@ cudaError_t launch_tma(const FlowArgs& a, cudaStream_t s) {
   if (smem > 48 * 1024 && cached < smem) {
     cudaError_t e = cudaFuncSetAttribute(flow_tma_kernel<T, MODE, NQ, LEARNED, WARPS, STAGES>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    // the whole unified L1/SMEM for shared memory, so that two SMEM-heavy CTAs fit per SM
+    e = cudaFuncSetAttribute(flow_tma_kernel<T, MODE, NQ, LEARNED, WARPS, STAGES>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     cached = smem;
   }

@@ -162,22 +162,36 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+// try_wait with a suspend-time hint: the waiting thread sleeps in the barrier unit until
+// the phase completes (or the hint, in ns, expires) instead of re-issuing polls that take
+// issue slots from the warps that have work
+#ifndef RLVLA_MBAR_HINT_NS
+#define RLVLA_MBAR_HINT_NS 1000000
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
+#if RLVLA_MBAR_HINT_NS > 0
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(RLVLA_MBAR_HINT_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
       " selp.u32 %0, 1, 0, p;\n}\n"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
-  return ok != 0;
+#endif
+  return ok != 0u;
 }
-// try_wait suspends in hardware for a bounded time per call (~us); 2^20 failed calls
-// (seconds) means a lost transaction: trap instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t n = 0;
+  // a phase that never completes traps after ~16 s (hinted waits) instead of hanging the GPU
   while (!mbar_try_wait(bar, parity)) {
-    if (++n > (1u << 20)) __trap();
+    if (++n > (RLVLA_MBAR_HINT_NS > 0 ? (1u << 14) : (1u << 20))) __trap();
   }
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {

@@ -26,6 +26,9 @@ enum { MODE_FWD = 0, MODE_FUSED = 1, MODE_BWD = 2 };
 #ifndef RLVLA_TGT_INLOOP
 #define RLVLA_TGT_INLOOP 0  // 1: the target dlogit merged into its vector inside pass C
 #endif
+#ifndef RLVLA_ISSUED_SLEEP_NS
+#define RLVLA_ISSUED_SLEEP_NS 64  // back-off of the stage-issue poll (0: spin)
+#endif
 #ifndef RLVLA_FUSED_NEGINF
 #define RLVLA_FUSED_NEGINF 1  // 0: the fused kernel skips the target inside the pass-B loop
 #endif
@@ -383,8 +386,12 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     // sure this row's load was issued (which happens only after that use was consumed).
     {
       uint32_t n = 0;
-      while (ld_volatile_s32(&meta[st].issued_row) != r)
+      while (ld_volatile_s32(&meta[st].issued_row) != r) {
+#if RLVLA_ISSUED_SLEEP_NS > 0
+        __nanosleep(RLVLA_ISSUED_SLEEP_NS);  // no issue slots taken from the other group
+#endif
         if (++n > (1u << 24)) __trap();
+      }
     }
     mbar_wait(&full[st], ph);
     uint8_t* row = rowbuf + size_t(st) * stage_bytes;

@@ -12,8 +12,9 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
+    "no16w": ("RLVLA_FLOW_16W_MINB=0",),
+    "nohint": ("RLVLA_MBAR_HINT_NS=0",),
     "s8x2": ("RLVLA_FLOW_SMALL_TILES=0",),
-    "direct": ("RLVLA_FLOW_TMA=0",),
 }
 # name -> git revision whose csrc/ + include/ are built as one more variant
 # (the ABI only grew at the end of its structs, so today's binding drives older libraries)
