@@ -561,8 +561,9 @@ __host__ __device__ constexpr int tma_ring_offset() {
 }
 
 template <typename T, int MODE, int NQ, bool LEARNED, int WARPS, int STAGES>
-// (16-warp CTAs are held to 64 registers so that two fit per SM with their SMEM rings:
-// one paper-sized update then has ~1.3 tiles per warp instead of ~2.6)
+// (RLVLA_FLOW_16W_MINB=1 holds 16-warp CTAs to 64 registers so that two fit per SM with their
+// SMEM rings — ~1.3 tiles per warp instead of ~2.6 for one paper-sized update; measured slower
+// from the spills it forces, so off)
 __global__ void __launch_bounds__(WARPS * 32, RLVLA_FLOW_16W_MINB && WARPS == 16 ? 2 : 1) flow_tma_kernel(FlowArgs a) {
   constexpr int kTmaWarps = WARPS, kFlowStages = STAGES;
   constexpr int n = 4 * NQ;

@@ -26,7 +26,7 @@ def main():
     ap.add_argument("--variant", default="none", choices=["none", "dual", "kl", "ent", "all"],
                     help="NEXT-2 loss knobs on the fused call (readings R19-R20)")
     a = ap.parse_args()
-    R, V, A = a.rows, a.vocab, a.A
+    R, V, A = a.rows - a.rows % a.A, a.vocab, a.A  # whole decision steps
     dev = "cuda"
     g = torch.Generator(device=dev).manual_seed(0)
     dt = torch.float32 if a.f32 else torch.bfloat16
