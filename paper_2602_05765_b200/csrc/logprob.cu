@@ -912,7 +912,14 @@ __device__ __forceinline__ void lse_merge(float& m, float& s, float& et, float m
 }
 
 template <typename T, int MODE>
-__global__ void __launch_bounds__(kRowThreads, 4) lp_row_kernel(Lp p) {
+#ifndef RLVLA_ROW_UNROLL
+#define RLVLA_ROW_UNROLL 2  // 16-byte vectors in flight per thread and loop trip
+#endif
+#ifndef RLVLA_ROW_MINB
+#define RLVLA_ROW_MINB 3    // resident CTAs per SM the register budget is sized for
+#endif
+__global__ void __launch_bounds__(kRowThreads, RLVLA_ROW_MINB) lp_row_kernel(Lp p) {
+  constexpr int U = RLVLA_ROW_UNROLL;
   constexpr int VN = RowVec<T>::kN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int V = p.V;
@@ -935,13 +942,26 @@ __global__ void __launch_bounds__(kRowThreads, 4) lp_row_kernel(Lp p) {
     if (MODE != MODE_BWD) {
       // ---- pass AB: online max / sum / entropy partial, the target column left out ------
       float m = -INFINITY, sm = 0.f, et = 0.f;
-      for (int v = tid; v < nvec; v += kRowThreads) {
-        float x[VN];
-        RowVec<T>::load(xr, v, x);
-        if (v == va) x[a - va * VN] = -INFINITY;
-        float lm = x[0];
+      for (int v0 = tid; v0 < nvec; v0 += U * kRowThreads) {
+        float x[U][VN];
+        float lm = -INFINITY;
 #pragma unroll
-        for (int j = 1; j < VN; ++j) lm = fmaxf(lm, x[j]);
+        for (int u = 0; u < U; ++u) {  // U loads in flight before any use
+          const int v = v0 + u * kRowThreads;
+          if (v < nvec) {
+            RowVec<T>::load(xr, v, x[u]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < VN; ++j) x[u][j] = -INFINITY;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int v = v0 + u * kRowThreads;
+          if (v == va) x[u][a - va * VN] = -INFINITY;
+#pragma unroll
+          for (int j = 0; j < VN; ++j) lm = fmaxf(lm, x[u][j]);
+        }
         if (lm > m) {  // the thread's max grows: rescale its partials
           const float d = (m == -INFINITY) ? 0.f : (m - lm) * L2E;
           const float f = (m == -INFINITY) ? 0.f : ex2(d);
@@ -951,12 +971,14 @@ __global__ void __launch_bounds__(kRowThreads, 4) lp_row_kernel(Lp p) {
         }
         const float nmL = (m == -INFINITY) ? 0.f : -m * L2E;
 #pragma unroll
-        for (int j = 0; j < VN; ++j) {
-          const float t = clamp_ninf(fmaf(x[j], L2E, nmL));
-          const float e = ex2(t);
-          sm += e;
-          et = fmaf(e, fmaxf(t, -256.f), et);
-        }
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int j = 0; j < VN; ++j) {
+            const float t = clamp_ninf(fmaf(x[u][j], L2E, nmL));
+            const float e = ex2(t);
+            sm += e;
+            et = fmaf(e, fmaxf(t, -256.f), et);
+          }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1)
@@ -1022,22 +1044,31 @@ __global__ void __launch_bounds__(kRowThreads, 4) lp_row_kernel(Lp p) {
       (void)Ms;
       T* dr = static_cast<T*>(p.dx) + r * p.ld;
       const float nML = -sc.M * L2E;
-      for (int v = tid; v < nvec; v += kRowThreads) {
-        float d[VN];
+      for (int v0 = tid; v0 < nvec; v0 += U * kRowThreads) {
+        float x[U][VN];
         if (sc.active != 0.f) {
-          float x[VN];
-          RowVec<T>::load(xr, v, x);
 #pragma unroll
-          for (int j = 0; j < VN; ++j) {
-            const float t = clamp_ninf(fmaf(x[j], L2E, nML));
-            d[j] = ex2(t) * fmaf(sc.k2, t, sc.k1);
-          }
-          if (v == va) d[a - va * VN] = sc.ga;
-        } else {
-#pragma unroll
-          for (int j = 0; j < VN; ++j) d[j] = 0.f;
+          for (int u = 0; u < U; ++u)  // U loads in flight (L2: the row was just read)
+            if (v0 + u * kRowThreads < nvec) RowVec<T>::load(xr, v0 + u * kRowThreads, x[u]);
         }
-        RowVec<T>::store(dr, v, d);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int v = v0 + u * kRowThreads;
+          if (v >= nvec) break;
+          float d[VN];
+          if (sc.active != 0.f) {
+#pragma unroll
+            for (int j = 0; j < VN; ++j) {
+              const float t = clamp_ninf(fmaf(x[u][j], L2E, nML));
+              d[j] = ex2(t) * fmaf(sc.k2, t, sc.k1);
+            }
+            if (v == va) d[a - va * VN] = sc.ga;
+          } else {
+#pragma unroll
+            for (int j = 0; j < VN; ++j) d[j] = 0.f;
+          }
+          RowVec<T>::store(dr, v, d);
+        }
       }
     }
     __syncthreads();  // red / rsc reuse across rows
@@ -1161,7 +1192,7 @@ cudaError_t launch_mode(const LpArgs& a, Lp p, cudaStream_t s) {
   }
   if (path == LP_PATH_ROW) {
     int64_t blocks = R;
-    const int64_t cap = int64_t(sms) * 4;
+    const int64_t cap = int64_t(sms) * RLVLA_ROW_MINB;
     if (blocks > cap) blocks = cap;
     if (a.x.dtype == RLVLA_BF16) lp_row_kernel<__nv_bfloat16, MODE><<<int(blocks), kRowThreads, 0, s>>>(p);
     else lp_row_kernel<float, MODE><<<int(blocks), kRowThreads, 0, s>>>(p);

@@ -12,9 +12,9 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
-    "no16w": ("RLVLA_FLOW_16W_MINB=0",),
-    "nohint": ("RLVLA_MBAR_HINT_NS=0",),
-    "s8x2": ("RLVLA_FLOW_SMALL_TILES=0",),
+    "u1m4": ("RLVLA_ROW_UNROLL=1", "RLVLA_ROW_MINB=4"),
+    "u2m4": ("RLVLA_ROW_MINB=4",),
+    "u4m2": ("RLVLA_ROW_UNROLL=4", "RLVLA_ROW_MINB=2"),
 }
 # name -> git revision whose csrc/ + include/ are built as one more variant
 # (the ABI only grew at the end of its structs, so today's binding drives older libraries)
@@ -79,6 +79,9 @@ def run(mode="fused", rounds=3):
             elif mode == "flow":
                 cmd = [sys.executable, os.path.join(ROOT, "tools", "prof_flow.py"), "--rows", "196608"]
                 cmd += os.environ.get("FLOW_ARGS", "").split()  # e.g. "--learned --f32"
+            elif mode.endswith("32"):  # fp32 logits (the row kernel): fused32 / fwd32 / bwd32
+                cmd = [sys.executable, os.path.join(ROOT, "tools", "prof_fused.py"), "--mode", mode[:-2],
+                       "--iters", "12", "--f32", "--rows", "32768"]
             else:
                 cmd = [sys.executable, os.path.join(ROOT, "tools", "prof_fused.py"), "--mode", mode,
                        "--iters", "12"]
