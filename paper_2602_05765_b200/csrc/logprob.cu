@@ -868,8 +868,8 @@ struct RowVec;
 template <>
 struct RowVec<float> {
   static constexpr int kN = 4;
-  __device__ __forceinline__ static void load(const void* row, int v, float (&x)[4]) {
-    const uint4 w = ldg_stream(reinterpret_cast<const uint4*>(row) + v);
+  __device__ __forceinline__ static void load(const void* row, int v, float (&x)[4], uint64_t pol) {
+    const uint4 w = ldg_hint(reinterpret_cast<const uint4*>(row) + v, pol);
     x[0] = __uint_as_float(w.x);
     x[1] = __uint_as_float(w.y);
     x[2] = __uint_as_float(w.z);
@@ -883,8 +883,8 @@ struct RowVec<float> {
 template <>
 struct RowVec<__nv_bfloat16> {
   static constexpr int kN = 8;
-  __device__ __forceinline__ static void load(const void* row, int v, float (&x)[8]) {
-    const uint4 w = ldg_stream(reinterpret_cast<const uint4*>(row) + v);
+  __device__ __forceinline__ static void load(const void* row, int v, float (&x)[8], uint64_t pol) {
+    const uint4 w = ldg_hint(reinterpret_cast<const uint4*>(row) + v, pol);
     const uint32_t w4[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -913,10 +913,13 @@ __device__ __forceinline__ void lse_merge(float& m, float& s, float& et, float m
 
 template <typename T, int MODE>
 #ifndef RLVLA_ROW_UNROLL
-#define RLVLA_ROW_UNROLL 2  // 16-byte vectors in flight per thread and loop trip
+#define RLVLA_ROW_UNROLL 4  // 16-byte vectors in flight per thread and loop trip
 #endif
 #ifndef RLVLA_ROW_MINB
-#define RLVLA_ROW_MINB 3    // resident CTAs per SM the register budget is sized for
+#define RLVLA_ROW_MINB 2    // resident CTAs per SM the register budget is sized for
+#endif
+#ifndef RLVLA_ROW_KEEP
+#define RLVLA_ROW_KEEP 1    // pass AB loads with L2 evict_last (re-read by pass C)
 #endif
 __global__ void __launch_bounds__(kRowThreads, RLVLA_ROW_MINB) lp_row_kernel(Lp p) {
   constexpr int U = RLVLA_ROW_UNROLL;
@@ -932,6 +935,10 @@ __global__ void __launch_bounds__(kRowThreads, RLVLA_ROW_MINB) lp_row_kernel(Lp 
   __shared__ RowScalars rsc;
   __shared__ double sacc[16];
   if (tid < 16) sacc[tid] = 0.0;
+  // pass AB's reads stay in L2 for pass C's re-read (evict_last), which is their last use
+  // (evict_first); external backward reads once (evict_first)
+  const uint64_t pol_last = policy_evict_first();
+  const uint64_t pol_keep = (MODE == MODE_FUSED && p.dx != nullptr && RLVLA_ROW_KEEP) ? policy_evict_last() : pol_last;
   __syncthreads();
   for (int64_t r = blockIdx.x; r < p.rows; r += gridDim.x) {
     const T* xr = static_cast<const T*>(p.x) + r * p.ld;
@@ -949,7 +956,7 @@ __global__ void __launch_bounds__(kRowThreads, RLVLA_ROW_MINB) lp_row_kernel(Lp 
         for (int u = 0; u < U; ++u) {  // U loads in flight before any use
           const int v = v0 + u * kRowThreads;
           if (v < nvec) {
-            RowVec<T>::load(xr, v, x[u]);
+            RowVec<T>::load(xr, v, x[u], pol_keep);
           } else {
 #pragma unroll
             for (int j = 0; j < VN; ++j) x[u][j] = -INFINITY;
@@ -1049,7 +1056,7 @@ __global__ void __launch_bounds__(kRowThreads, RLVLA_ROW_MINB) lp_row_kernel(Lp 
         if (sc.active != 0.f) {
 #pragma unroll
           for (int u = 0; u < U; ++u)  // U loads in flight (L2: the row was just read)
-            if (v0 + u * kRowThreads < nvec) RowVec<T>::load(xr, v0 + u * kRowThreads, x[u]);
+            if (v0 + u * kRowThreads < nvec) RowVec<T>::load(xr, v0 + u * kRowThreads, x[u], pol_last);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {

@@ -258,9 +258,13 @@ def test_fullsize_microbatched_configs(name):
         oadv = H.oracle_advantages(case, obuf, "gae", whiten=cfg.whiten)
         H.assert_close_rel(adv.cpu().numpy(), oadv["adv"], 1e-5, 1.0, "adv (gae)")
     assert stats[3].item() == oadv["counts"]["n_tok"]
-    a32 = adv.cpu().numpy().astype(np.float64)
-    tv = O_path.token_view(obuf, a32, A, synth.CUR_VERSION)
-    N = stats[3].item()
+    # the GPU chain runs on its own advantages and N_tok, the oracle chain on its own (S2's
+    # tolerance propagated as in tests/test_parity_path.py)
+    from tests.test_parity_path import check_rows
+    floor = max(1e-3, float(np.sqrt(np.mean(oadv["adv"] ** 2))))
+    tol_tok = np.repeat((1e-5 * np.maximum(np.abs(oadv["adv"]), floor)).reshape(-1), A)
+    tv = O_path.token_view(obuf, oadv["adv"], A, synth.CUR_VERSION)
+    N = float(oadv["counts"]["n_tok"])
     for e0, e1 in tested:
         lo, hi = e0 * env_rows, e1 * env_rows
         xmb = synth.gen_logits(cfg, traj, e0, e1, device="cuda")
@@ -277,13 +281,10 @@ def test_fullsize_microbatched_configs(name):
                                 stats=st, ws=ws)
         torch.cuda.synchronize()
         rows = samples[(e0, e1)]
-        x = xmb[torch.from_numpy(rows - lo).cuda()].double().cpu().numpy()
-        ref = O_path.loss_and_grad(x, tv, n_tok=N, rows=rows)
-        H.assert_close_rel(logp.cpu().numpy()[rows - lo], ref["fwd"]["logp"], 1e-5, 1.0, "logp")
-        nt = ref["ppo"]["near_tie"]
-        H.assert_close_rel(g.cpu().numpy()[rows - lo][~nt], ref["ppo"]["grad"][~nt], 1e-5, 1e-9, "grad")
-        bits = dx[torch.from_numpy(rows - lo).cuda()].view(torch.int16).cpu().numpy().astype(np.int32) & 0xFFFF
-        H.assert_bf16_ulp(bits[~nt], ref["dx"][~nt], 1)
+        li = torch.from_numpy(rows - lo).cuda()
+        x = xmb[li].double().cpu().numpy()
+        check_rows(x, dict(logp=logp.cpu().numpy()[rows - lo], g=g.cpu().numpy()[rows - lo], dx=dx[li]),
+                   tv, rows, N, tol_tok[rows], xmb.dtype)
         # the call's token count = the oracle's masked tokens of this micro-batch
         allr = np.arange(lo, hi)
         base = tv["valid"][allr] & (tv["target"][allr] >= 0) & (tv["lag"][allr] >= 0) & (tv["lag"][allr] <= 1)

@@ -12,9 +12,8 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
-    "u1m4": ("RLVLA_ROW_UNROLL=1", "RLVLA_ROW_MINB=4"),
-    "u2m4": ("RLVLA_ROW_MINB=4",),
-    "u4m2": ("RLVLA_ROW_UNROLL=4", "RLVLA_ROW_MINB=2"),
+    "nokeep": ("RLVLA_ROW_KEEP=0",),
+    "u2keep": ("RLVLA_ROW_UNROLL=2", "RLVLA_ROW_MINB=3"),
 }
 # name -> git revision whose csrc/ + include/ are built as one more variant
 # (the ABI only grew at the end of its structs, so today's binding drives older libraries)
