@@ -546,6 +546,12 @@ __global__ void __launch_bounds__(kFlowWarps * 32, RLVLA_FLOW_MINB) flow_kernel(
 #ifndef RLVLA_FLOW_16W_MINB
 #define RLVLA_FLOW_16W_MINB 0  // 1: cap the 16-warp shape at 64 registers (2 CTAs per SM; A/B: spills, slower)
 #endif
+#ifndef RLVLA_FLOW_L2_LEAD
+#define RLVLA_FLOW_L2_LEAD 0  // 1: L2 prefetch of the next tile beyond the SMEM ring (A/B: slower)
+#endif
+#ifndef RLVLA_FLOW_SMALL_WARPS
+#define RLVLA_FLOW_SMALL_WARPS 16  // warps of the single-stage small-call shape (16, 12 or 8)
+#endif
 #ifndef RLVLA_FLOW_SMALL_TILES
 #define RLVLA_FLOW_SMALL_TILES 9472  // tiles below which the 16 x 1 shape runs (0: never)
 #endif
@@ -597,8 +603,18 @@ __global__ void __launch_bounds__(WARPS * 32, RLVLA_FLOW_16W_MINB && WARPS == 16
     bulk_g2s(st + kMuB, a.c.x + e0, kXB, bar, pol);
     if (LEARNED) bulk_g2s(st + kMuB + kXB, a.c.log_std + e0, kXB, bar, pol);
   };
-  if (lane == 0)
+  // L2 lead: the tile after the ones in the SMEM ring is prefetched into L2 (bulk prefetch,
+  // no SMEM), so its TMA fill — issued only once a stage frees up — is an L2 hit
+  auto prefetch = [&](int64_t i) {
+    const int64_t e0 = (gw + i * nw) * kTile * n;
+    bulk_prefetch_l2(mu0 + e0, uint32_t(kMuB));
+    bulk_prefetch_l2(a.c.x + e0, uint32_t(kXB));
+    if (LEARNED) bulk_prefetch_l2(a.c.log_std + e0, uint32_t(kXB));
+  };
+  if (lane == 0) {
     for (int64_t i = 0; i < cnt && i < kFlowStages; ++i) issue(i);
+    if (RLVLA_FLOW_L2_LEAD && kFlowStages < cnt) prefetch(kFlowStages);
+  }
   float gin;
   RowMeta4 mt_next = load_meta<MODE>(a, x, gw < nfull ? gw * kTile : 0, kTile, lane, gin);
   for (int64_t i = 0; i < cnt; ++i) {
@@ -620,7 +636,10 @@ __global__ void __launch_bounds__(WARPS * 32, RLVLA_FLOW_16W_MINB && WARPS == 16
     // the stage's generic-proxy reads and rewrites are ordered before its next TMA fill
     fence_proxy_async();
     __syncwarp();
-    if (lane == 0 && i + kFlowStages < cnt) issue(i + kFlowStages);
+    if (lane == 0 && i + kFlowStages < cnt) {
+      issue(i + kFlowStages);
+      if (RLVLA_FLOW_L2_LEAD && i + kFlowStages + 1 < cnt) prefetch(i + kFlowStages + 1);
+    }
   }
   const int64_t tail = a.c.rows - nfull * kTile;
   if (tail > 0 && gw == nfull % nw)
@@ -712,7 +731,8 @@ cudaError_t launch_q(const FlowArgs& a, cudaStream_t s) {
         (!a.c.log_std || reinterpret_cast<uintptr_t>(a.c.log_std) % 16 == 0)) {
       const int mode = a.grad_logp ? 2 : a.fused ? 1 : 0;
       if (a.c.log_std != nullptr) return launch_tma_m<T, NQ, true, 4, 2>(a, s, mode);
-      if ((a.c.rows + kTile - 1) / kTile < RLVLA_FLOW_SMALL_TILES) return launch_tma_m<T, NQ, false, 16, 1>(a, s, mode);
+      if ((a.c.rows + kTile - 1) / kTile < RLVLA_FLOW_SMALL_TILES)
+        return launch_tma_m<T, NQ, false, RLVLA_FLOW_SMALL_WARPS, 1>(a, s, mode);
       return launch_tma_m<T, NQ, false, 8, 2>(a, s, mode);
     }
   }

@@ -26,6 +26,9 @@ enum { MODE_FWD = 0, MODE_FUSED = 1, MODE_BWD = 2 };
 #ifndef RLVLA_TGT_INLOOP
 #define RLVLA_TGT_INLOOP 0  // 1: the target dlogit merged into its vector inside pass C
 #endif
+#ifndef RLVLA_L2_PREFETCH
+#define RLVLA_L2_PREFETCH 0  // 1: L2 prefetch of the row a stage is refilled with, a row ahead (A/B: slower)
+#endif
 #ifndef RLVLA_ISSUED_SLEEP_NS
 #define RLVLA_ISSUED_SLEEP_NS 64  // back-off of the stage-issue poll (0: spin)
 #endif
@@ -393,6 +396,14 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
         if (++n > (1u << 24)) __trap();
       }
     }
+#if RLVLA_L2_PREFETCH
+    // the row this group loads into its stage at the end of this row (row k + nstages) is
+    // pulled into L2 now, a row-time ahead, so that TMA fill is an L2 hit: the SMEM ring
+    // holds only three 64 KB rows, L2 extends the prefetch depth
+    if (gt == 0 && k + nstages < nrow)
+      bulk_prefetch_l2(static_cast<const __nv_bfloat16*>(p.x) + int64_t(first + (k + nstages) * stride) * p.ld,
+                       row_bytes);
+#endif
     mbar_wait(&full[st], ph);
     uint8_t* row = rowbuf + size_t(st) * stage_bytes;
     uint4* rv = reinterpret_cast<uint4*>(row);
