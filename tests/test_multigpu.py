@@ -21,16 +21,18 @@ def _port():
 
 
 @pytest.mark.parametrize("n,mode", [(2, "p2p"), (2, "nccl"), (4, "p2p"), (4, "nccl"),
-                                    (4, "p2p-only"), (8, "p2p-only")])
+                                    (2, "p2p-only"), (4, "p2p-only"), (8, "p2p-only")])
 def test_multigpu_parity(n, mode):
     """The loss statistics reduced in-kernel over NVLink peer memory (RLVLA_P2P=1, the
     default), through NCCL (RLVLA_P2P=0), and with the P2P-only communicator (no NCCL; a gloo
-    group exchanges the IPC handles, ranks round-robin over the GPUs, so 8 ranks run on 4
-    GPUs at the mailbox's full 8-rank capacity) all match the oracle."""
+    group exchanges the IPC handles, ranks round-robin over the GPUs, so 8 ranks run on 4 —
+    or on 1 — GPUs at the mailbox's full 8-rank capacity) all match the oracle."""
     ndev = torch.cuda.device_count()
     if mode == "p2p-only":
-        if ndev < 2 or n > 4 * ndev:
-            pytest.skip(f"needs >= 2 GPUs and <= 4 ranks per GPU (have {ndev})")
+        # several ranks per GPU (time-sliced contexts): the logical-shard mode of SURVEY §4.2,
+        # so a one-GPU box still runs the in-kernel multi-rank exchange
+        if ndev < 1 or n > 8 * ndev:
+            pytest.skip(f"needs <= 8 ranks per GPU (have {ndev} GPUs)")
     elif ndev < n:
         pytest.skip(f"needs {n} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
