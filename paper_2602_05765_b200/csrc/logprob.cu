@@ -38,6 +38,9 @@ enum { MODE_FWD = 0, MODE_FUSED = 1, MODE_BWD = 2 };
 #ifndef RLVLA_PASSC_BF16
 #define RLVLA_PASSC_BF16 1  // 0: pass C in fp32 (unpack, FMUL2, pack) instead of bf16 HFMA2
 #endif
+#ifndef RLVLA_DX_BULK
+#define RLVLA_DX_BULK 0  // 1: pass C writes dlogits into the stage, one TMA bulk store per row
+#endif
 #ifndef RLVLA_NFULL_FUSED
 #define RLVLA_NFULL_FUSED 1  // 0: every vector of the fused kernel bounds-checked
 #endif
@@ -615,23 +618,40 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
                 if (z == qd) ow[z] = hf ? ((ow[z] & 0x0000ffffu) | (hb << 16)) : ((ow[z] & 0xffff0000u) | hb);
             }
 #endif
+#if RLVLA_DX_BULK
+            rv[idx] = o;  // in place: this thread's own vector, read above
+#else
             stg_stream(dv + idx, o);
+#endif
           }
         }
 #if !RLVLA_TGT_INLOOP
         // the target column (0 from its -inf above) takes g (1 - p_a) [+ ...]: stored by
         // the thread that stored its vector, after it (same-thread order)
-        if (owner) reinterpret_cast<uint16_t*>(drow)[a] = __bfloat16_as_ushort(__float2bfloat16_rn(rsv.ga));
+        if (owner)
+          reinterpret_cast<uint16_t*>(RLVLA_DX_BULK ? static_cast<void*>(row) : static_cast<void*>(drow))[a] =
+              __bfloat16_as_ushort(__float2bfloat16_rn(rsv.ga));
 #endif
       } else {
 #pragma unroll
         for (int i = 0; i < kVecPerThread; ++i) {
           const int idx = gt + i * kGroupThreads;
+#if RLVLA_DX_BULK
+          if (i < NFULL || idx < nvec) rv[idx] = make_uint4(0u, 0u, 0u, 0u);
+#else
           if (i < NFULL || idx < nvec) stg_stream(dv + idx, make_uint4(0u, 0u, 0u, 0u));
+#endif
         }
       }
     }
     group_sync(grp);  // #3: stage fully consumed by this group
+#if RLVLA_DX_BULK
+    if (has_c && gt == 0) {  // the row's dlogits leave the stage in one bulk store
+      fence_proxy_async();
+      bulk_s2g(static_cast<__nv_bfloat16*>(p.dx) + int64_t(r) * p.ld, row, row_bytes, pol);
+      if (k + nstages < nrow) bulk_wait_read();  // before the stage is refilled
+    }
+#endif
     if (gt == 0 && k + nstages < nrow) {
       fence_proxy_async();
       issue_row<MODE>(p, first + (k + nstages) * stride, row, &meta[st], &full[st], row_bytes, pol);
@@ -639,6 +659,9 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     advance_stage(st, ph, nstages);
   }
 
+#if RLVLA_DX_BULK
+  if (has_c && gt == 0) bulk_wait_all();
+#endif
   if (want_stats) {
     __syncthreads();
     if (tid < kLossSlots) gacc[tid] += gacc[16 + tid];  // fixed order: group 0 then group 1
