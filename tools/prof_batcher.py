@@ -82,6 +82,20 @@ def main():
     torch.cuda.synchronize()
     idle = [e[0].elapsed_time(e[1]) for e in evs]
     ref = [e[1].elapsed_time(e[2]) for e in evs]
+    # the same timing around a one-element torch kernel: the event + launch floor of a
+    # single call after the flush (what an idle poll is compared with)
+    one = torch.zeros(1, device="cuda")
+    torch.cuda._sleep(200_000_000)
+    evs = []
+    for i in range(a.iters):
+        flush.sum()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record(s)
+        one.add_(1.0)
+        ev[1].record(s)
+        evs.append(ev)
+    torch.cuda.synchronize()
+    floor = sorted(e[0].elapsed_time(e[1]) for e in evs)
     # steady tick loop: offer B ready envs + one firing poll per tick, back to back (PDL
     # overlaps each launch with the previous kernel); slots of n_env_loop envs exceed L2
     E2 = max(E, (512 << 20) // ob + 1)
@@ -137,6 +151,7 @@ def main():
                       "poll_us_min": min(poll_ms) * 1e3, "offer_us_median": sorted(offer_ms)[len(offer_ms) // 2] * 1e3,
                       "GBps_median": byts / pm / 1e6, "GBps_best": byts / min(poll_ms) / 1e6,
                       "idle_poll_us_median": sorted(idle)[len(idle) // 2] * 1e3,
+                      "floor_us_median": floor[len(floor) // 2] * 1e3,
                       "torch_index_select_us_median": sorted(ref)[len(ref) // 2] * 1e3,
                       "tick_loop": {"n_env": E2, "us_per_tick": tick_us, "GBps": byts / tick_us / 1e3},
                       "staged_tick_loop": staged,

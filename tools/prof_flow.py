@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--learned", action="store_true", help="learned ln sigma (+ its gradient)")
     ap.add_argument("--f32", action="store_true", help="fp32 means (default bf16)")
+    ap.add_argument("--no-stats", action="store_true", help="no loss statistics (no last-CTA reduction)")
+    ap.add_argument("--fwd", action="store_true", help="chain log-likelihood only (no PPO, no backward)")
     a = ap.parse_args()
     R, K, D = a.rows, a.K, a.D
     g = torch.Generator(device="cuda").manual_seed(0)
@@ -48,7 +50,11 @@ def main():
     flush = torch.zeros(64 << 20, dtype=torch.float32, device="cuda")
 
     def call():
-        P.rlvla_flow_logprob(ch, logp=logp, fused=fa, dmu=dmu, dlog_std=dls, stats=st, ws=ws)
+        if a.fwd:
+            P.rlvla_flow_logprob(ch, logp=logp)
+        else:
+            P.rlvla_flow_logprob(ch, logp=logp, fused=fa, dmu=dmu, dlog_std=dls,
+                                 stats=None if a.no_stats else st, ws=ws)
 
     for _ in range(3):
         call()
@@ -64,15 +70,32 @@ def main():
         evs.append(e)
     torch.cuda.synchronize()
     ms = sorted(e[0].elapsed_time(e[1]) for e in evs)
+    # the same timing around a one-element torch kernel: the event + launch floor
+    one = torch.zeros(1, device="cuda")
+    torch.cuda._sleep(100_000_000)
+    fe = []
+    for _ in range(a.iters):
+        flush.sum()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        e[0].record()
+        one.add_(1.0)
+        e[1].record()
+        fe.append(e)
+    torch.cuda.synchronize()
+    floor = sorted(e[0].elapsed_time(e[1]) for e in fe)
     n = R * K * D
     eb = mu.element_size()
     byts = n * (eb + 4 + (4 if a.learned else 0)) + n * (eb + (4 if a.learned else 0)) + R * (4 + 4 + 4 + 4 + 8 + 4)
     med = ms[len(ms) // 2]
-    print(json.dumps({"what": "rlvla_flow_logprob fused PPO + backward", "rows": R, "K": K, "D": D,
+    if a.fwd:
+        byts = n * (eb + 4 + (4 if a.learned else 0)) + R * 4
+    print(json.dumps({"what": "rlvla_flow_logprob " + ("forward only" if a.fwd else "fused PPO + backward")
+                      + (", no stats" if a.no_stats else ""), "rows": R, "K": K, "D": D,
                       "mu_dtype": str(mdt).replace("torch.", ""), "learned_log_std": a.learned,
                       "alg_bytes": byts, "us_median": med * 1e3, "us_min": ms[0] * 1e3,
                       "GBps_median": byts / med / 1e6, "GBps_best": byts / ms[0] / 1e6,
-                      "loss": float(st[6].item())}))
+                      "loss": float(st[6].item()), "ms_all": [round(v * 1e3, 2) for v in ms],
+                      "floor_us_median": floor[len(floor) // 2] * 1e3}))
 
 
 if __name__ == "__main__":
