@@ -12,7 +12,6 @@ sys.path.insert(0, ROOT)
 VAR = os.path.join(ROOT, "paper_2602_05765_b200", "variants")
 VARIANTS = {
     "base": (),
-    "fenceall": ("RLVLA_FENCE_WRITERS=0",),
 }
 # name -> git revision whose csrc/ + include/ are built as one more variant
 # (the ABI only grew at the end of its structs, so today's binding drives older libraries)
