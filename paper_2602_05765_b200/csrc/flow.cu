@@ -503,6 +503,9 @@ __device__ __forceinline__ void flow_finish(const FlowArgs& a, const FlowCtx& x,
                     MODE == 1 ? a.f.accumulate : 0, MODE == 1 ? a.f.ent_coef : 0.f, &a.ws.p2p);
 }
 
+#ifndef RLVLA_FLOW_LOADPOL
+#define RLVLA_FLOW_LOADPOL 0  // TMA tile loads: 0 L2 evict_first, 1 evict_normal
+#endif
 #ifndef RLVLA_FLOW_MINB
 #define RLVLA_FLOW_MINB 4  // resident CTAs per SM the register budget is sized for
 #endif
@@ -593,7 +596,11 @@ __global__ void __launch_bounds__(WARPS * 32, RLVLA_FLOW_16W_MINB && WARPS == 16
   const int64_t gw = int64_t(blockIdx.x) * kTmaWarps + warp, nw = int64_t(gridDim.x) * kTmaWarps;
   const int64_t cnt = gw < nfull ? (nfull - gw + nw - 1) / nw : 0;  // this warp's full tiles
   const T* const mu0 = static_cast<const T*>(a.c.mu);
+#if RLVLA_FLOW_LOADPOL
+  const uint64_t pol = policy_evict_normal();
+#else
   const uint64_t pol = policy_evict_first();
+#endif
   auto issue = [&](int64_t i) {  // lane 0: tile gw + i nw -> stage i % kFlowStages
     const int64_t e0 = (gw + i * nw) * kTile * n;
     unsigned char* st = ring + (i % kFlowStages) * stage_b;

@@ -38,6 +38,18 @@ enum { MODE_FWD = 0, MODE_FUSED = 1, MODE_BWD = 2 };
 #ifndef RLVLA_PASSC_BF16
 #define RLVLA_PASSC_BF16 1  // 0: pass C in fp32 (unpack, FMUL2, pack) instead of bf16 HFMA2
 #endif
+#ifndef RLVLA_RING_ONLY
+#define RLVLA_RING_ONLY 0  // 1: diagnostic, TMA ring + stores only (results wrong; A/B ceiling)
+#endif
+#ifndef RLVLA_TMA_STG
+#define RLVLA_TMA_STG 1  // dlogits stores of the TMA kernel: 0 st.global.cs, 1 st.global (wb), 2 st.global.L1::no_allocate
+#endif
+#ifndef RLVLA_TMA_LOADPOL
+#define RLVLA_TMA_LOADPOL 1  // TMA row loads: 0 L2 evict_first, 1 evict_normal, 2 no hint, 3 evict_last, 4 evict_unchanged
+#endif
+#ifndef RLVLA_ROW_LOADPOL
+#define RLVLA_ROW_LOADPOL 0  // row kernel's last-use loads: 0 L2 evict_first, 1 evict_normal
+#endif
 #ifndef RLVLA_DX_BULK
 #define RLVLA_DX_BULK 0  // 1: pass C writes dlogits into the stage, one TMA bulk store per row
 #endif
@@ -46,6 +58,19 @@ enum { MODE_FWD = 0, MODE_FUSED = 1, MODE_BWD = 2 };
 #endif
 
 constexpr uint32_t kNegClampPair = 0xF180F180u;  // bf16x2 (-2^100, -2^100)
+
+__device__ __forceinline__ void stg_dx(uint4* p, uint4 v) {
+#if RLVLA_TMA_STG == 1
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+#elif RLVLA_TMA_STG == 2
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+#else
+  stg_stream(p, v);
+#endif
+}
 
 // -inf -> -1e30, NaN kept (a comparison with NaN is false)
 __device__ __forceinline__ float clamp_ninf(float t) { return t < -1e30f ? -1e30f : t; }
@@ -301,7 +326,15 @@ __device__ __forceinline__ void issue_row(const Lp& p, int r, uint8_t* dst, Stag
   }
   cp_async_arrive_noinc(bar);
   mbar_arrive_expect_tx(bar, row_bytes);
+#if RLVLA_TMA_LOADPOL == 2  // no L2 cache hint on the row copy
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(static_cast<const __nv_bfloat16*>(p.x) + int64_t(r) * p.ld), "r"(row_bytes), "r"(smem_u32(bar))
+               : "memory");
+  (void)pol;
+#else
   bulk_g2s(dst, static_cast<const __nv_bfloat16*>(p.x) + int64_t(r) * p.ld, row_bytes, bar, pol);
+#endif
 }
 
 __device__ __forceinline__ void group_sync(int g) {
@@ -373,7 +406,18 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
   if (tid < 32) gacc[tid] = 0.0;
   if (tid < kMaxStages) meta[tid].issued_row = -1;
   __syncthreads();
+#if RLVLA_TMA_LOADPOL == 1
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#elif RLVLA_TMA_LOADPOL == 3
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#elif RLVLA_TMA_LOADPOL == 4
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(pol));
+#else
   uint64_t pol = policy_evict_first();
+#endif
   if (tid == 0) {
     const int pre = nrow < nstages ? nrow : nstages;
     for (int k = 0; k < pre; ++k)
@@ -410,6 +454,25 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     mbar_wait(&full[st], ph);
     uint8_t* row = rowbuf + size_t(st) * stage_bytes;
     uint4* rv = reinterpret_cast<uint4*>(row);
+#if RLVLA_RING_ONLY
+    // diagnostic build (wrong results): the TMA ring and the dlogits stores alone, no math —
+    // the ceiling of this kernel's memory structure
+    if (has_c) {
+      uint4* dvr = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.dx) + int64_t(r) * p.ld);
+#pragma unroll
+      for (int i = 0; i < kVecPerThread; ++i) {
+        const int idx = gt + i * kGroupThreads;
+        if (i < NFULL || idx < nvec) stg_dx(dvr + idx, rv[idx]);
+      }
+    }
+    group_sync(grp);
+    if (gt == 0 && k + nstages < nrow) {
+      fence_proxy_async();
+      issue_row<MODE>(p, first + (k + nstages) * stride, row, &meta[st], &full[st], row_bytes, pol);
+    }
+    advance_stage(st, ph, nstages);
+    continue;
+#endif
     const StageMeta* mt = &meta[st];
     const int a = mt->a;
     const bool tgt_ok = unsigned(a) < unsigned(V);
@@ -621,7 +684,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
 #if RLVLA_DX_BULK
             rv[idx] = o;  // in place: this thread's own vector, read above
 #else
-            stg_stream(dv + idx, o);
+            stg_dx(dv + idx, o);
 #endif
           }
         }
@@ -639,7 +702,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
 #if RLVLA_DX_BULK
           if (i < NFULL || idx < nvec) rv[idx] = make_uint4(0u, 0u, 0u, 0u);
 #else
-          if (i < NFULL || idx < nvec) stg_stream(dv + idx, make_uint4(0u, 0u, 0u, 0u));
+          if (i < NFULL || idx < nvec) stg_dx(dv + idx, make_uint4(0u, 0u, 0u, 0u));
 #endif
         }
       }
@@ -971,7 +1034,11 @@ __global__ void __launch_bounds__(kRowThreads, RLVLA_ROW_MINB) lp_row_kernel(Lp 
   if (tid < 16) sacc[tid] = 0.0;
   // pass AB's reads stay in L2 for pass C's re-read (evict_last), which is their last use
   // (evict_first); external backward reads once (evict_first)
+#if RLVLA_ROW_LOADPOL
+  const uint64_t pol_last = policy_evict_normal();
+#else
   const uint64_t pol_last = policy_evict_first();
+#endif
   const uint64_t pol_keep = (MODE == MODE_FUSED && p.dx != nullptr && RLVLA_ROW_KEEP) ? policy_evict_last() : pol_last;
   __syncthreads();
   for (int64_t r = blockIdx.x; r < p.rows; r += gridDim.x) {

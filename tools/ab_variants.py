@@ -15,7 +15,7 @@ VARIANTS = {
 }
 # name -> git revision whose csrc/ + include/ are built as one more variant
 # (the ABI only grew at the end of its structs, so today's binding drives older libraries)
-REVISIONS = {"prev": os.environ.get("AB_PREV", "HEAD")}  # the last commit as a variant
+REVISIONS = {"prev": os.environ.get("AB_PREV", "HEAD")} if os.environ.get("AB_PREV", "HEAD") != "none" else {}  # the last commit as a variant
 
 
 def build_revision(name, rev):

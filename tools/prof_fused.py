@@ -17,7 +17,8 @@ import paper_2602_05765_b200 as P  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--mode", default="fused", choices=["fused", "fwd", "bwd"])
+    ap.add_argument("--mode", default="fused", choices=["fused", "fwd", "bwd", "copy"],
+                    help="copy: torch's dx.copy_(x) of the same bytes (the copy ceiling at this size)")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--rows", type=int, default=229376)
     ap.add_argument("--vocab", type=int, default=32000)
@@ -64,6 +65,8 @@ def main():
     def call():
         if a.mode == "fused":
             P.rlvla_logprob_fwd_bwd(x, t, logp=logp, fused=fa, dlogits=dx, stats=stats, ws=ws)
+        elif a.mode == "copy":
+            dx.copy_(x)
         elif a.mode == "fwd":
             P.rlvla_logprob_fwd_bwd(x, t, logp=logp, lse=lse)
         else:
@@ -80,7 +83,7 @@ def main():
         ev[i + 1].record()
     torch.cuda.synchronize()
     ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(a.iters)]
-    rw = {"fused": 2 * V * esz + 12, "fwd": V * esz + 12, "bwd": 2 * V * esz + 12}[a.mode]
+    rw = {"copy": 2 * V * esz, "fused": 2 * V * esz + 12, "fwd": V * esz + 12, "bwd": 2 * V * esz + 12}[a.mode]
     if a.mode == "fused" and "logp_ref" in vk:
         rw += 4
     byt = R * rw
