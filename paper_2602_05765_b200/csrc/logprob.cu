@@ -50,6 +50,9 @@ enum { MODE_FWD = 0, MODE_FUSED = 1, MODE_BWD = 2 };
 #ifndef RLVLA_ROW_LOADPOL
 #define RLVLA_ROW_LOADPOL 0  // row kernel's last-use loads: 0 L2 evict_first, 1 evict_normal
 #endif
+#ifndef RLVLA_TMA_SPLIT
+#define RLVLA_TMA_SPLIT 1  // bulk copies per row (A/B)
+#endif
 #ifndef RLVLA_DX_BULK
 #define RLVLA_DX_BULK 0  // 1: pass C writes dlogits into the stage, one TMA bulk store per row
 #endif
@@ -332,6 +335,13 @@ __device__ __forceinline__ void issue_row(const Lp& p, int r, uint8_t* dst, Stag
                "l"(static_cast<const __nv_bfloat16*>(p.x) + int64_t(r) * p.ld), "r"(row_bytes), "r"(smem_u32(bar))
                : "memory");
   (void)pol;
+#elif RLVLA_TMA_SPLIT > 1  // the row as several bulk copies on the same mbarrier
+  {
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(static_cast<const __nv_bfloat16*>(p.x) + int64_t(r) * p.ld);
+    const uint32_t part = ((row_bytes / RLVLA_TMA_SPLIT) + 15u) & ~15u;
+    for (uint32_t o = 0; o < row_bytes; o += part)
+      bulk_g2s(dst + o, src + o, row_bytes - o < part ? row_bytes - o : part, bar, pol);
+  }
 #else
   bulk_g2s(dst, static_cast<const __nv_bfloat16*>(p.x) + int64_t(r) * p.ld, row_bytes, bar, pol);
 #endif
